@@ -1,0 +1,88 @@
+/* fms_oracle.h -- plain fp64 CPU oracle of Faster Mean-shift (arXiv 2007.14283).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  It shares no code, header, table or constant
+ * generator with the CUDA path (paper_2007_14283_b200/), and neither includes the other.
+ *
+ * Every function follows the paper step by step (PAPER.md line numbers "P:n"); where the paper is
+ * silent or garbled the reading is the DESIGN.md "Readings" entry named R#.
+ * All floating point is fp64; summation orders are fixed (ascending pixel index), so results are
+ * bitwise identical for any OpenMP thread count.
+ */
+#ifndef FMS_ORACLE_H
+#define FMS_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { FMSO_OK = 0, FMSO_E_INVALID = 2, FMSO_E_ZERO_NORM = 3, FMSO_E_STALLED = 4, FMSO_E_CAPACITY = 5 };
+enum { FMSO_SEEDS_FIXED = 0, FMSO_SEEDS_OSOP = 1, FMSO_SEEDS_ALL = 2 };
+#define FMSO_MAX_ROUNDS 16
+
+typedef struct {
+  int32_t kind;            /* FMSO_SEEDS_* */
+  int32_t n_seeds;         /* FIXED: seed count; OSOP: N_initial (128) */
+  double gamma;            /* early-stop fraction (0.9) */
+  double L, H, P;          /* OSOP controller (2, 8) and coverage target (0.99) */
+  int32_t has_background;  /* largest cluster is background when estimating I, r (R14) */
+  int32_t min_instance_px; /* clusters smaller than this do not count toward I (R22) */
+  int32_t saturation_stop; /* stop when a round adds no counted instance (R22) */
+  int32_t max_rounds;      /* <= FMSO_MAX_ROUNDS */
+  uint64_t rng_seed;       /* hash-priority selection salt (R11) */
+} fmso_policy;
+
+typedef struct {
+  int32_t rounds, K;
+  int64_t seeds_total, seed_iters, discarded;
+  int32_t round_K[FMSO_MAX_ROUNDS];      /* seeds launched in round r (K_r) */
+  int32_t round_iters[FMSO_MAX_ROUNDS];  /* lockstep iterations run */
+  int32_t round_conv[FMSO_MAX_ROUNDS];   /* converged seeds */
+  int32_t round_disc[FMSO_MAX_ROUNDS];   /* discarded (unconverged / stalled) seeds */
+  int64_t round_seed_iters[FMSO_MAX_ROUNDS]; /* sum over t of active seeds A_t */
+  int32_t round_Kc[FMSO_MAX_ROUNDS];     /* centres after merge */
+  int32_t round_I[FMSO_MAX_ROUNDS];      /* observed instance count (OSOP) */
+  int64_t round_cand[FMSO_MAX_ROUNDS];   /* uncovered & unvisited pixels after assignment */
+  double round_r[FMSO_MAX_ROUNDS];       /* observed foreground ratio */
+  double round_nmin[FMSO_MAX_ROUNDS];    /* N_min (Eq. 19); -1 = infinite */
+} fmso_trace;
+
+/* ---- scalar pieces (P8/P9 pins) ---- */
+uint64_t fmso_splitmix64(uint64_t z);
+uint64_t fmso_key(uint64_t rng_seed, int32_t round, int64_t i);
+double fmso_p_success(int64_t N, int64_t I, double r);      /* Eq. 14 */
+int64_t fmso_n_min(double P, int64_t I, double r);           /* Eq. 19; INT64_MAX if I == 0 */
+int32_t fmso_need(double gamma, int64_t K);                  /* ceil(gamma*K) (R8) */
+
+/* ---- vector pieces ---- */
+int fmso_normalize(const float* emb, int64_t n, int32_t d, double* xhat);         /* Eq. 1 / 9 */
+int64_t fmso_select(const uint8_t* cand, int64_t n, int64_t K, uint64_t rng_seed,
+                    int32_t round, int64_t* out);                                 /* Alg. 2 l.2 */
+int64_t fmso_window(const double* xhat, int64_t n, int32_t d, double tau,
+                    const double* s, double* g);                                  /* Eq. 8+11 */
+/* Lockstep mean-shift over K seeds (Alg. 2 l.4-9 + early stop).  seeds[K*d] in/out, status[K]:
+ * 1 converged, 2 stalled, 3 discarded.  Returns iterations run; writes intensity (window count of
+ * the final update, R10) and per-seed iteration count. */
+int32_t fmso_lockstep(const double* xhat, int64_t n, int32_t d, double h, int32_t max_iter,
+                      double tol, double gamma, int64_t K, double* seeds, uint8_t* status,
+                      int64_t* intensity, int32_t* iters, int64_t* seed_iters);
+/* Greedy merge (R10): pool rows sorted by (intensity desc, origin asc), keep unless within rho of
+ * a kept centre.  Writes kept indices into keep[] in kept order; returns the kept count. */
+int64_t fmso_merge(const double* pool, const int64_t* intensity, const int64_t* origin,
+                   int64_t m, int32_t d, double rho, int64_t* keep);
+/* Nearest-mode assignment (Alg. 2 l.12-14): label = argmax_k x.c_k (lowest k on ties). */
+void fmso_assign(const double* xhat, int64_t n, int32_t d, const double* centres, int64_t K,
+                 double tau, int32_t* labels, uint8_t* covered, int64_t* hist);
+
+/* ---- full method ---- */
+int fmso_cluster(const float* emb, int64_t n, int32_t d, double h, int32_t max_iter, double tol,
+                 const fmso_policy* pol, int32_t* labels, double* centres, int32_t centres_cap,
+                 int32_t* K_out, fmso_trace* trace);
+
+int fmso_num_threads(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
