@@ -1,0 +1,127 @@
+/* fms.h -- C ABI of the B200 (sm_100a) Faster Mean-shift hot path (arXiv 2007.14283).
+ *
+ * The library clusters unit-normalised pixel embeddings with the paper's Faster Mean-shift:
+ * batched lockstep mean-shift of seed vectors with a flat cosine kernel (Alg. 2, PAPER.md
+ * P:179-223), online seed optimisation (OSOP, Eq. 12-21), merging of converged modes
+ * ("pruned and merged if their distance is small") and nearest-mode assignment of every
+ * pixel (Alg. 2 l.12-14).  Readings of the paper are listed in DESIGN.md ("R#").
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Device pointers are CUDA global-memory addresses on the
+ *    context's device; host pointers are ordinary (preferably pinned) host memory.
+ *  - The caller owns every input and output buffer.  Inputs are read-only and never retained
+ *    after a call returns.  The context owns its workspace (grown on demand).
+ *  - Every call returns an fms_status; nothing aborts.  fms_last_error(ctx) gives a message.
+ *  - A context may be used by one host thread at a time; distinct contexts are independent.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Calls are
+ *    stream-ordered and return once results are complete (K_out is a host value).
+ *  - Limits of this build: 1 <= d <= 32 (rows are padded to 16 or 32 fp16 lanes), n < 2^31/B.
+ */
+#ifndef FMS_H
+#define FMS_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FMS_OK = 0,
+  FMS_E_INVALID = 2,   /* usage: n<1, d<1 or d>32, h not in (0,1), tol<=0, max_iters<1, bad policy ("2") */
+  FMS_E_ZERO_NORM = 3, /* a row has zero or non-finite norm: no direction (Eq. 9 needs |x|>0; "3") */
+  FMS_E_STALLED = 4,   /* no seed converged in round 0 ("4") */
+  FMS_E_CAPACITY = 5,  /* K > centres_cap (labels still valid; *K_out = required K) or an internal capacity */
+  FMS_E_CUDA = 6,      /* CUDA runtime / launch error; message in fms_last_error */
+  FMS_E_NCCL = 7,      /* reserved for the multi-GPU paths */
+  FMS_E_OOM = 8,       /* workspace allocation failed */
+  FMS_E_INTERNAL = 9   /* internal consistency check failed */
+} fms_status;
+
+typedef enum {
+  FMS_SEEDS_FIXED = 0, /* exactly n_seeds seeds, one round */
+  FMS_SEEDS_OSOP = 1,  /* online seed optimisation (readings R12-R15, R22) */
+  FMS_SEEDS_ALL = 2    /* every pixel is a seed, gamma = 1: Alg. 1 */
+} fms_seed_kind;
+
+/* Seed policy.  Defaults (fms_default_policy): OSOP, N_initial = 128, gamma = 0.9,
+ * L = 2, H = 8, P = 0.99, background on, min_instance_px = 0, saturation off,
+ * max_rounds = 8, rng_seed = 0. */
+typedef struct {
+  int32_t kind;            /* fms_seed_kind */
+  int32_t n_seeds;         /* FIXED: seed count; OSOP: N_initial */
+  double gamma;            /* early stop once ceil(gamma*K_r) seeds converged (R8), 0 < gamma <= 1 */
+  double L, H, P;          /* OSOP: stop once seeds >= L*N_min (Eq. 21); H (session only); coverage target (Eq. 19) */
+  int32_t has_background;  /* 1: the largest cluster is background when observing I, r (R14) */
+  int32_t min_instance_px; /* clusters smaller than this do not count toward I (R22); 0 = paper */
+  int32_t saturation_stop; /* 1: stop when a round adds no counted instance (R22) */
+  int32_t max_rounds;      /* 1..16 */
+  uint64_t rng_seed;       /* salt of the seed-selection hash (R11) */
+} fms_seed_policy;
+
+#define FMS_MAX_ROUNDS 16
+
+/* Per-frame trace (identical fields to the test oracle's trace; counts are the run's own work). */
+typedef struct {
+  int32_t status, rounds, K, pad;
+  int64_t seeds_total, seed_iters, discarded;
+  int32_t round_K[FMS_MAX_ROUNDS];     /* seeds launched in round r */
+  int32_t round_iters[FMS_MAX_ROUNDS]; /* lockstep iterations run in round r */
+  int32_t round_conv[FMS_MAX_ROUNDS];
+  int32_t round_disc[FMS_MAX_ROUNDS];
+  int32_t round_Kc[FMS_MAX_ROUNDS];    /* centres after the merge of round r */
+  int32_t round_I[FMS_MAX_ROUNDS];
+  int64_t round_seed_iters[FMS_MAX_ROUNDS]; /* sum over t of active seeds */
+  int64_t round_cand[FMS_MAX_ROUNDS];  /* uncovered & unvisited pixels after assignment */
+  double round_r[FMS_MAX_ROUNDS];
+  double round_nmin[FMS_MAX_ROUNDS];   /* N_min of Eq. 19, -1 = infinite */
+} fms_frame_stats;
+
+/* Per-call counters (whole batch). */
+typedef struct {
+  double ms_total;            /* wall time of the call on the stream (CUDA events) */
+  int64_t workspace_bytes;    /* device workspace owned by the context */
+  int32_t steps;              /* lockstep steps launched (including no-op tail steps) */
+  int32_t iter_launches;      /* K2 launches that had work */
+  double iter_ms;             /* summed K2 device time over those launches (only if profiling on) */
+  int64_t iter_seed_iters;    /* sum over K2 launches of active seeds (units of work) */
+  int64_t iter_items;         /* sum over K2 launches of work items */
+} fms_run_stats;
+
+fms_status fms_default_policy(fms_seed_policy* out);
+
+fms_status fms_ctx_create(void** ctx_out, int device);
+void fms_ctx_destroy(void* ctx);
+const char* fms_last_error(const void* ctx);
+const char* fms_version(void);
+
+/* Options: "profile_iter" (0/1): time every K2 launch with CUDA events for fms_run_stats.iter_ms. */
+fms_status fms_set_option(void* ctx, const char* key, int64_t value);
+
+/* Cluster one frame.  emb: device, [n][d] fp32 row-major.  labels: device int32[n] in [0, K).
+ * centres: device fp32 [centres_cap][d], unit rows in merge order (intensity desc, origin asc).
+ * K_out: host.  frame_stats/run_stats: host, nullable. */
+fms_status fms_cluster(void* ctx, const float* emb, int64_t n, int32_t d, double bandwidth, int32_t max_iters,
+                       double tol, const fms_seed_policy* policy, int32_t* labels, float* centres,
+                       int32_t centres_cap, int32_t* K_out, fms_frame_stats* frame_stats,
+                       fms_run_stats* run_stats, void* stream);
+
+/* Cluster B independent frames of identical shape in one pass (the throughput entry point).
+ * emb: device [B][n][d]; labels: device [B][n]; centres: device [B][centres_cap][d];
+ * K_out: host int32[B]; frame_stats: host [B] or NULL.  Frames never interact. */
+fms_status fms_cluster_batch(void* ctx, const float* emb, int32_t B, int64_t n, int32_t d, double bandwidth,
+                             int32_t max_iters, double tol, const fms_seed_policy* policy, int32_t* labels,
+                             float* centres, int32_t centres_cap, int32_t* K_out, fms_frame_stats* frame_stats,
+                             fms_run_stats* run_stats, void* stream);
+
+/* Same as fms_cluster_batch with HOST buffers: the embeddings are copied to the device, and labels /
+ * centres copied back, inside the call (end-to-end entry).  Pinned host memory is recommended. */
+fms_status fms_cluster_batch_host(void* ctx, const float* emb_host, int32_t B, int64_t n, int32_t d,
+                                  double bandwidth, int32_t max_iters, double tol,
+                                  const fms_seed_policy* policy, int32_t* labels_host, float* centres_host,
+                                  int32_t centres_cap, int32_t* K_out, fms_frame_stats* frame_stats,
+                                  fms_run_stats* run_stats, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

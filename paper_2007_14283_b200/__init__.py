@@ -1,0 +1,198 @@
+"""Python binding of libfms.so, the B200 (sm_100a) Faster Mean-shift hot path.
+
+Argument marshalling only: every step of the method runs in the CUDA kernels behind the C ABI
+(include/fms.h).  There is no CPU or PyTorch fallback: if the library is missing or no sm_100
+device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+SEEDS_FIXED, SEEDS_OSOP, SEEDS_ALL = 0, 1, 2
+MAX_ROUNDS = 16
+STATUS = {0: "OK", 2: "INVALID", 3: "ZERO_NORM", 4: "STALLED", 5: "CAPACITY", 6: "CUDA", 7: "NCCL", 8: "OOM",
+          9: "INTERNAL"}
+EXPORTS = ["fms_default_policy", "fms_ctx_create", "fms_ctx_destroy", "fms_last_error", "fms_version",
+           "fms_set_option", "fms_cluster", "fms_cluster_batch", "fms_cluster_batch_host"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfms.so")
+
+
+class Policy(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n_seeds", C.c_int32), ("gamma", C.c_double), ("L", C.c_double),
+                ("H", C.c_double), ("P", C.c_double), ("has_background", C.c_int32),
+                ("min_instance_px", C.c_int32), ("saturation_stop", C.c_int32), ("max_rounds", C.c_int32),
+                ("rng_seed", C.c_uint64)]
+
+
+class FrameStats(C.Structure):
+    _fields_ = [("status", C.c_int32), ("rounds", C.c_int32), ("K", C.c_int32), ("pad", C.c_int32),
+                ("seeds_total", C.c_int64), ("seed_iters", C.c_int64), ("discarded", C.c_int64),
+                ("round_K", C.c_int32 * MAX_ROUNDS), ("round_iters", C.c_int32 * MAX_ROUNDS),
+                ("round_conv", C.c_int32 * MAX_ROUNDS), ("round_disc", C.c_int32 * MAX_ROUNDS),
+                ("round_Kc", C.c_int32 * MAX_ROUNDS), ("round_I", C.c_int32 * MAX_ROUNDS),
+                ("round_seed_iters", C.c_int64 * MAX_ROUNDS), ("round_cand", C.c_int64 * MAX_ROUNDS),
+                ("round_r", C.c_double * MAX_ROUNDS), ("round_nmin", C.c_double * MAX_ROUNDS)]
+
+    def as_dict(self) -> dict:
+        R = self.rounds
+        return dict(status=self.status, rounds=R, K=self.K, seeds_total=self.seeds_total,
+                    seed_iters=self.seed_iters, discarded=self.discarded,
+                    round_K=list(self.round_K[:R]), round_iters=list(self.round_iters[:R]),
+                    round_conv=list(self.round_conv[:R]), round_disc=list(self.round_disc[:R]),
+                    round_seed_iters=list(self.round_seed_iters[:R]), round_Kc=list(self.round_Kc[:R]),
+                    round_I=list(self.round_I[:R]), round_cand=list(self.round_cand[:R]),
+                    round_r=list(self.round_r[:R]), round_nmin=list(self.round_nmin[:R]))
+
+
+class RunStats(C.Structure):
+    _fields_ = [("ms_total", C.c_double), ("workspace_bytes", C.c_int64), ("steps", C.c_int32),
+                ("iter_launches", C.c_int32), ("iter_ms", C.c_double), ("iter_seed_iters", C.c_int64),
+                ("iter_items", C.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libfms.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2007_14283_b200.build` "
+                              "(no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        L.fms_version.restype = C.c_char_p
+        L.fms_last_error.restype = C.c_char_p
+        L.fms_last_error.argtypes = [vp]
+        L.fms_default_policy.argtypes = [C.POINTER(Policy)]
+        L.fms_ctx_create.argtypes = [C.POINTER(vp), C.c_int]
+        L.fms_ctx_destroy.argtypes = [vp]
+        L.fms_ctx_destroy.restype = None
+        L.fms_set_option.argtypes = [vp, C.c_char_p, i64]
+        common = [f64, i32, f64, C.POINTER(Policy), vp, vp, i32, vp, vp, C.POINTER(RunStats), vp]
+        L.fms_cluster.argtypes = [vp, vp, i64, i32] + common
+        L.fms_cluster_batch.argtypes = [vp, vp, i32, i64, i32] + common
+        L.fms_cluster_batch_host.argtypes = [vp, vp, i32, i64, i32] + common
+        for fn in ("fms_default_policy", "fms_ctx_create", "fms_set_option", "fms_cluster", "fms_cluster_batch",
+                   "fms_cluster_batch_host"):
+            getattr(L, fn).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def default_policy(**kw) -> Policy:
+    p = Policy()
+    lib().fms_default_policy(C.byref(p))
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+class FmsError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"fms status {status} ({STATUS.get(status, '?')}): {msg}")
+        self.status = status
+
+
+class Context:
+    """One fms context (device workspace, TMA descriptors) on one CUDA device."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = C.c_void_p()
+        rc = lib().fms_ctx_create(C.byref(h), device)
+        if rc != 0:
+            raise FmsError(rc, f"fms_ctx_create(device={device}) failed (needs an sm_100 GPU)")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().fms_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_option(self, key: str, value: int):
+        self._check(lib().fms_set_option(self.h, key.encode(), int(value)))
+
+    def _check(self, rc: int, allow=()):
+        if rc != 0 and rc not in allow:
+            raise FmsError(rc, lib().fms_last_error(self.h).decode())
+        return rc
+
+    def cluster_batch_ptr(self, emb_ptr: int, B: int, n: int, d: int, labels_ptr: int, centres_ptr: int,
+                          centres_cap: int, h: float = 0.1, max_iters: int = 300, tol: float | None = None,
+                          policy: Policy | None = None, stream: int = 0, allow=()):
+        """Raw-pointer entry (device pointers).  Returns (status, K[B], frame stats, run stats)."""
+        tol = h / 1000.0 if tol is None else tol
+        policy = policy if policy is not None else default_policy()
+        K = (C.c_int32 * B)()
+        fs = (FrameStats * B)()
+        rs = RunStats()
+        rc = lib().fms_cluster_batch(self.h, C.c_void_p(emb_ptr), B, n, d, h, max_iters, tol, C.byref(policy),
+                                     C.c_void_p(labels_ptr), C.c_void_p(centres_ptr), centres_cap, K, fs,
+                                     C.byref(rs), C.c_void_p(stream))
+        self._check(rc, allow)
+        return rc, list(K), [f.as_dict() for f in fs], rs.as_dict()
+
+    def cluster(self, emb, h: float = 0.1, max_iters: int = 300, tol: float | None = None,
+                policy: Policy | None = None, centres_cap: int = 4096, allow=()):
+        """emb: torch CUDA float32 tensor [n, d] or [B, n, d].  Returns (labels, centres, K, stats).
+        labels: int32 [B, n]; centres: float32 [B, centres_cap, d] (rows < K valid)."""
+        import torch
+        if emb.dim() == 2:
+            emb = emb.unsqueeze(0)
+        if not (emb.is_cuda and emb.dtype == torch.float32):
+            raise TypeError("emb must be a CUDA float32 tensor")
+        emb = emb.contiguous()
+        B, n, d = emb.shape
+        labels = torch.empty((B, n), dtype=torch.int32, device=emb.device)
+        centres = torch.zeros((B, max(centres_cap, 1), d), dtype=torch.float32, device=emb.device)
+        stream = torch.cuda.current_stream(emb.device).cuda_stream
+        rc, K, fs, rs = self.cluster_batch_ptr(emb.data_ptr(), B, n, d, labels.data_ptr(), centres.data_ptr(),
+                                               centres_cap, h, max_iters, tol, policy, stream, allow)
+        return labels, centres, K, dict(status=rc, frames=fs, run=rs)
+
+    def cluster_host(self, emb_host, labels_host, centres_host, centres_cap: int, h: float = 0.1,
+                     max_iters: int = 300, tol: float | None = None, policy: Policy | None = None, stream: int = 0,
+                     allow=()):
+        """Host-buffer entry (end-to-end): emb_host [B,n,d] float32, labels_host [B,n] int32,
+        centres_host [B,cap,d] float32 -- all pinned CPU torch tensors (or anything with data_ptr())."""
+        B, n, d = emb_host.shape
+        tol = h / 1000.0 if tol is None else tol
+        policy = policy if policy is not None else default_policy()
+        K = (C.c_int32 * B)()
+        rs = RunStats()
+        rc = lib().fms_cluster_batch_host(self.h, C.c_void_p(emb_host.data_ptr()), B, n, d, h, max_iters, tol,
+                                          C.byref(policy), C.c_void_p(labels_host.data_ptr()),
+                                          C.c_void_p(centres_host.data_ptr()), centres_cap, K, None,
+                                          C.byref(rs), C.c_void_p(stream))
+        self._check(rc, allow)
+        return rc, list(K), rs.as_dict()
+
+
+_ctxs: dict[int, Context] = {}
+
+
+def context(device: int = 0) -> Context:
+    if device not in _ctxs:
+        _ctxs[device] = Context(device)
+    return _ctxs[device]
+
+
+def cluster(emb, h: float = 0.1, max_iters: int = 300, tol: float | None = None, policy: Policy | None = None,
+            centres_cap: int = 4096, allow=()):
+    """Cluster one frame [n, d] or a batch [B, n, d] of CUDA float32 embeddings (see Context.cluster)."""
+    return context(emb.device.index or 0).cluster(emb, h, max_iters, tol, policy, centres_cap, allow)

@@ -1,0 +1,315 @@
+// k_post.cu -- per-round post-processing: K4 merge, K5 assignment + coverage, K7 OSOP control.
+//
+// K4 ("modes are further pruned and merged if their distance is small"; reading R10):
+//     pool = previous centres U this round's converged modes; order by (intensity desc, origin asc);
+//     greedy: keep a mode unless a kept centre lies within cosine distance rho = h.  Kept modes are
+//     not averaged.  One CTA per frame: bitonic sort of the pool keys in SMEM, then the greedy scan in
+//     batches of 32 candidates (all kept-vs-candidate tests of a batch in parallel, the in-batch
+//     chain resolved by one warp with ballots).
+// K5 (Alg. 2 l.12-14): label = argmax_k x.c_k (lowest k on ties, R21); covered =
+//     max_k x_hat.c_k >= tau; per-centre histogram; count of uncovered & unvisited pixels.
+//     fp32 FMA on the fp32 input (HBM-bound scan; full-precision decisions for coverage).
+// K7 (Eq. 12-19; readings R12-R15, R22): background = largest cluster,
+//     I = #other clusters with >= min_instance_px pixels, r = 1 - |bg|/n,
+//     N_min = ceil( ln(1 - e^{ln P / I}) / ln(1 - r/I) ); stop when coverage holds
+//     (no candidates / total >= L N_min / total >= n / max_rounds / saturation), else double N.
+#include "fms_device.cuh"
+
+namespace fms {
+
+template <int DP>
+__device__ __forceinline__ float dotv(const float* a, const float* b) {
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < DP; ++k) s = fmaf(a[k], b[k], s);
+  return s;
+}
+
+template <int DP>
+__global__ void __launch_bounds__(1024) merge_kernel(Params p) {
+  const int f = blockIdx.x;
+  FrameCtl& c = p.ctl[f];
+  if (c.phase != PH_POST) return;
+  extern __shared__ uint8_t dsm[];
+  __shared__ int sm[33];
+  __shared__ unsigned s_supp;
+  __shared__ int s_kept, s_err;
+
+  const int Kc = c.Kc;
+  const int K = c.K_r;
+  const int P = Kc + c.n_conv;
+  if (P > p.P_cap) {
+    if (threadIdx.x == 0) { c.status = 5; c.phase = PH_ERROR; }
+    return;
+  }
+  float* pool = p.pool + (size_t)f * p.P_cap * DP;
+  int* pint = p.pint + (size_t)f * p.P_cap;
+  int* porg = p.porg + (size_t)f * p.P_cap;
+  float* cent = p.cent + (size_t)f * p.C_cap * DP;
+  // 1. assemble the pool: previous centres, then this round's converged seeds (seed order)
+  for (int k = threadIdx.x; k < Kc; k += blockDim.x) {
+    for (int q = 0; q < DP; ++q) pool[(size_t)k * DP + q] = cent[(size_t)k * DP + q];
+    pint[k] = p.cint[(size_t)f * p.C_cap + k];
+    porg[k] = p.corig[(size_t)f * p.C_cap + k];
+  }
+  const size_t sb = (size_t)f * p.S_cap;
+  int carry = Kc;
+  for (int j0 = 0; j0 < K; j0 += blockDim.x) {
+    const int j = j0 + threadIdx.x;
+    const int a = (j < K && p.sstat[sb + j] == ST_CONV) ? 1 : 0;
+    int tot;
+    const int pos = carry + block_excl_scan(a, sm, &tot);
+    if (a) {
+      for (int q = 0; q < DP; ++q) pool[(size_t)pos * DP + q] = p.seeds[(sb + j) * DP + q];
+      pint[pos] = p.scnt[sb + j];
+      porg[pos] = p.sorig[sb + j];
+    }
+    carry += tot;
+  }
+  // 2. sort keys (intensity desc, origin asc) -- bitonic in SMEM
+  int P2 = 1;
+  while (P2 < P) P2 <<= 1;
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(dsm);
+  int* vals = reinterpret_cast<int*>(keys + P2);
+  __syncthreads();
+  for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+    if (i < P) {
+      keys[i] = ((unsigned long long)(0x7FFFFFFFu - (unsigned)pint[i]) << 32) | (unsigned)porg[i];
+      vals[i] = i;
+    } else {
+      keys[i] = ~0ull;
+      vals[i] = -1;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const unsigned long long a = keys[i], b = keys[ixj];
+          if ((a > b) == up) {
+            keys[i] = b; keys[ixj] = a;
+            const int t = vals[i]; vals[i] = vals[ixj]; vals[ixj] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // 3. greedy NMS in batches of 32
+  const float thr = p.rho_f;  // keep unless x.c >= 1 - rho
+  if (threadIdx.x == 0) { s_kept = 0; s_err = 0; }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int base = 0; base < P; base += 32) {
+    const int nb = min(32, P - base);
+    if (threadIdx.x == 0) s_supp = 0;
+    __syncthreads();
+    const int kept = s_kept;
+    const int total = nb * kept;
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+      const int ci = idx / kept, k = idx - ci * kept;
+      if (dotv<DP>(pool + (size_t)vals[base + ci] * DP, cent + (size_t)k * DP) >= thr) atomicOr(&s_supp, 1u << ci);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const float* a = lane < nb ? pool + (size_t)vals[base + lane] * DP : pool;
+      unsigned inb = 0;
+      for (int j = 0; j < nb; ++j)
+        if (j < lane && dotv<DP>(a, pool + (size_t)vals[base + j] * DP) >= thr) inb |= 1u << j;
+      const unsigned supp = s_supp;
+      unsigned keep = 0;
+      for (int i = 0; i < nb; ++i) {
+        const int ok = (lane == i) && !((supp >> i) & 1u) && !(inb & keep);
+        if (__ballot_sync(0xffffffffu, ok)) keep |= 1u << i;
+      }
+      if (lane < nb && ((keep >> lane) & 1u)) {
+        const int pos = kept + __popc(keep & ((1u << lane) - 1u));
+        if (pos < p.C_cap) {
+          for (int q = 0; q < DP; ++q) cent[(size_t)pos * DP + q] = a[q];
+          p.cint[(size_t)f * p.C_cap + pos] = pint[vals[base + lane]];
+          p.corig[(size_t)f * p.C_cap + pos] = porg[vals[base + lane]];
+        } else {
+          s_err = 1;
+        }
+      }
+      if (lane == 0) s_kept = kept + __popc(keep);
+    }
+    __syncthreads();
+  }
+  const int Kn = s_kept;
+  for (int k = threadIdx.x; k < Kn && k < p.C_cap; k += blockDim.x) p.hist[(size_t)f * p.C_cap + k] = 0;
+  if (threadIdx.x == 0) {
+    if (s_err) { c.status = 5; c.phase = PH_ERROR; }
+    c.Kc = Kn < p.C_cap ? Kn : p.C_cap;
+    c.ncand = 0;
+  }
+}
+
+
+template <int DP>
+__global__ void __launch_bounds__(256) assign_kernel(Params p) {
+  constexpr int kAsgChunk = 8192 / DP;  // centres per SMEM chunk (32 KB)
+  const int f = blockIdx.y;
+  FrameCtl& c = p.ctl[f];
+  if (c.phase != PH_POST) return;
+  __shared__ float sc[kAsgChunk * DP];
+  __shared__ int sh[kAsgChunk];
+  __shared__ int s_cand;
+  const int Kc = c.Kc;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i < p.n;
+  float x[DP];
+#pragma unroll
+  for (int k = 0; k < DP; ++k) x[k] = 0.f;
+  if (valid) {
+    const float* src = p.emb + ((size_t)f * p.n + i) * p.d;
+#pragma unroll
+    for (int k = 0; k < DP; ++k)
+      if (k < p.d) x[k] = src[k];
+  }
+  if (threadIdx.x == 0) s_cand = 0;
+  float best = -INFINITY;
+  int lab = 0;
+  const float* cent = p.cent + (size_t)f * p.C_cap * DP;
+  for (int k0 = 0; k0 < Kc; k0 += kAsgChunk) {
+    const int nk = min(kAsgChunk, Kc - k0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nk * DP; t += blockDim.x) sc[t] = cent[(size_t)k0 * DP + t];
+    __syncthreads();
+    for (int k = 0; k < nk; ++k) {
+      const float dv = dotv<DP>(x, sc + k * DP);
+      if (dv > best) { best = dv; lab = k0 + k; }
+    }
+  }
+  // histogram of labels (SMEM per chunk of centres), coverage and candidate count
+  int cand = 0;
+  if (valid) {
+    const size_t pi = (size_t)f * p.n + i;
+    const bool covered = best * p.inv[pi] >= p.tau_f;
+    const uint8_t fl = p.flags[pi];
+    p.flags[pi] = (uint8_t)((fl & ~PF_COVERED) | (covered ? PF_COVERED : 0));
+    p.labels[pi] = lab;
+    cand = (!covered && !(fl & PF_VISITED)) ? 1 : 0;
+  }
+  for (int k0 = 0; k0 < Kc; k0 += kAsgChunk) {
+    const int nk = min(kAsgChunk, Kc - k0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nk; t += blockDim.x) sh[t] = 0;
+    __syncthreads();
+    if (valid && lab >= k0 && lab < k0 + nk) atomicAdd(&sh[lab - k0], 1);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nk; t += blockDim.x)
+      if (sh[t]) atomicAdd(&p.hist[(size_t)f * p.C_cap + k0 + t], sh[t]);
+  }
+  cand = __syncthreads_count(cand);
+  if (threadIdx.x == 0 && cand) atomicAdd((unsigned long long*)&c.ncand, (unsigned long long)cand);
+}
+
+__global__ void osop_kernel(Params p) {
+  __shared__ int sm[33];
+  int not_done = 0;
+  for (int f0 = 0; f0 < p.B; f0 += blockDim.x) {
+    const int f = f0 + threadIdx.x;
+    if (f < p.B) {
+      FrameCtl& c = p.ctl[f];
+      if (c.phase == PH_POST) {
+        const int r = c.round;
+        c.round_Kc[r] = c.Kc;
+        c.round_cand[r] = c.ncand;
+        if (p.kind != 1 /*OSOP*/) {
+          c.phase = PH_DONE;
+        } else {
+          const int* hist = p.hist + (size_t)f * p.C_cap;
+          int bg = -1;
+          if (p.has_bg) {
+            bg = 0;
+            for (int k = 1; k < c.Kc; ++k)
+              if (hist[k] > hist[bg]) bg = k;
+          }
+          int I = 0;
+          for (int k = 0; k < c.Kc; ++k)
+            if (k != bg && hist[k] >= p.min_px) ++I;
+          const double rr = bg >= 0 ? 1.0 - (double)hist[bg] / (double)p.n : 1.0;
+          double nmin = -1.0;  // -1 = infinite (no instance observed)
+          if (I > 0 && rr > 0.0) {
+            const double q = rr / (double)I;
+            if (q >= 1.0) {
+              nmin = 1.0;
+            } else {
+              double v = ceil(log(-expm1(log(p.P) / (double)I)) / log1p(-q));
+              nmin = v < 1.0 ? 1.0 : v;
+            }
+          }
+          c.round_I[r] = I;
+          c.round_r[r] = rr;
+          c.round_nmin[r] = nmin;
+          const bool stop = c.ncand == 0 || c.total >= p.n || r + 1 >= p.max_rounds ||
+                            (nmin > 0.0 && (double)c.total >= p.L * nmin) ||
+                            (p.sat_stop && r >= 1 && I <= c.I_prev);
+          c.I_prev = I;
+          if (stop) {
+            c.phase = PH_DONE;
+          } else {
+            c.K_next = c.total < c.ncand ? c.total : c.ncand;
+            c.round = r + 1;
+            c.phase = PH_SELECT;
+          }
+        }
+      }
+      if (c.phase == PH_SELECT || c.phase == PH_ITERATE || c.phase == PH_POST) not_done = 1;
+    }
+  }
+  int tot;
+  block_excl_scan(not_done, sm, &tot);
+  if (threadIdx.x == 0) p.counters[2] = tot;
+}
+
+template <int DP>
+__global__ void output_kernel(Params p, float* centres_out, int cap) {
+  const int f = blockIdx.y;
+  const FrameCtl& c = p.ctl[f];
+  const int Kc = c.Kc < cap ? c.Kc : cap;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < Kc * p.d; t += gridDim.x * blockDim.x) {
+    const int k = t / p.d, q = t - k * p.d;
+    centres_out[((size_t)f * cap + k) * p.d + q] = p.cent[((size_t)f * p.C_cap + k) * DP + q];
+  }
+}
+
+int merge_smem_bytes(int P_cap) {
+  int P2 = 1;
+  while (P2 < P_cap) P2 <<= 1;
+  return P2 * 12;
+}
+
+cudaError_t setup_post_attrs(int P_cap) {
+  const int sm = merge_smem_bytes(P_cap);
+  cudaError_t e = cudaFuncSetAttribute(merge_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(merge_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+}
+
+cudaError_t launch_post(const Params& p, cudaStream_t st) {
+  const int sm = merge_smem_bytes(p.P_cap);
+  dim3 ga((unsigned)((p.n + 255) / 256), p.B);
+  if (p.DP == 16) {
+    merge_kernel<16><<<p.B, 1024, sm, st>>>(p);
+    assign_kernel<16><<<ga, 256, 0, st>>>(p);
+  } else {
+    merge_kernel<32><<<p.B, 1024, sm, st>>>(p);
+    assign_kernel<32><<<ga, 256, 0, st>>>(p);
+  }
+  osop_kernel<<<1, 1024, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_output(const Params& p, float* centres_out, int cap, cudaStream_t st) {
+  dim3 g(32, p.B);
+  if (p.DP == 16) output_kernel<16><<<g, 256, 0, st>>>(p, centres_out, cap);
+  else output_kernel<32><<<g, 256, 0, st>>>(p, centres_out, cap);
+  return cudaGetLastError();
+}
+
+}  // namespace fms

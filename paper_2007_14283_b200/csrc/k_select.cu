@@ -1,0 +1,321 @@
+// k_select.cu -- K1 (normalise + quantise) and K6 (OSOP seed selection).
+//
+// K1: Eq. 1 / Eq. 9 -- every embedding is divided by its norm; the
+//     unit vector is stored in fp16 as the tensor-core operand (row padded to DP, frame padded to a
+//     whole number of 128-pixel tiles with zero rows, which never enter a window since tau > 0).
+// K6: Alg. 2 line 2 ("Evenly random select seed vector set"), reading R11: the K_r candidate
+//     pixels with the smallest splitmix64 keys, in ascending pixel order.  Candidates are all pixels
+//     in round 0 and the uncovered, unvisited pixels afterwards (north_star / R13).
+//     Exact K-smallest selection without a sort of all n keys:
+//       collect  -- every candidate whose key is below a threshold T sized for ~K + 4 sqrt(K) + 64
+//                   survivors is appended to a per-frame sample (warp-aggregated atomics)
+//       kth      -- one CTA per frame finds the K-th smallest sampled key by 8-bit MSD radix select
+//                   (falls back to a radix select over all candidates if the sample was too small)
+//       count / scan / write -- ordered stream compaction of {candidate, key <= kth} -> seeds
+#include "fms_device.cuh"
+
+namespace fms {
+
+// ------------------------------------------------------------------------------------------------
+__global__ void init_ctl_kernel(Params p) {
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= p.B) return;
+  FrameCtl& c = p.ctl[f];
+  memset(&c, 0, sizeof(FrameCtl));
+  c.phase = PH_SELECT;
+  c.I_prev = -1;
+  for (int r = 0; r < kMaxRounds; ++r) c.round_nmin[r] = 0.0;
+}
+
+template <int DP>
+__global__ void prep_kernel(Params p) {
+  const int f = blockIdx.y;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n_pad) return;
+  __align__(16) __half h[DP];
+  if (i < p.n) {
+    const float* x = p.emb + ((size_t)f * p.n + i) * p.d;
+    float v[DP];
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < DP; ++k) {
+      v[k] = k < p.d ? x[k] : 0.f;
+      ss = fmaf(v[k], v[k], ss);
+    }
+    const float nrm = sqrtf(ss);
+    float inv = 0.f;
+    if (!(nrm > 0.f) || !isfinite(nrm)) {
+      atomicExch(&p.ctl[f].status, 3 /*FMS_E_ZERO_NORM*/);
+    } else {
+      inv = 1.0f / nrm;
+    }
+#pragma unroll
+    for (int k = 0; k < DP; ++k) h[k] = __float2half_rn(v[k] * inv);
+    p.inv[(size_t)f * p.n + i] = inv;
+    p.flags[(size_t)f * p.n + i] = 0;
+  } else {
+#pragma unroll
+    for (int k = 0; k < DP; ++k) h[k] = __float2half_rn(0.f);
+  }
+  uint4* dst = reinterpret_cast<uint4*>(p.Xh + ((size_t)f * p.n_pad + i) * DP);
+  const uint4* src = reinterpret_cast<const uint4*>(h);
+#pragma unroll
+  for (int k = 0; k < DP / 8; ++k) dst[k] = src[k];
+}
+
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool is_candidate(const Params& p, int f, int round, long long i) {
+  if (round == 0) return true;
+  return (p.flags[(size_t)f * p.n + i] & (PF_VISITED | PF_COVERED)) == 0;
+}
+
+__global__ void sel_prepare_kernel(Params p) {
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= p.B) return;
+  FrameCtl& c = p.ctl[f];
+  if (c.phase != PH_SELECT) return;
+  if (c.status != 0) { c.phase = PH_ERROR; return; }
+  long long ncand, Kreq;
+  if (c.round == 0) {
+    ncand = p.n;
+    Kreq = p.kind == 2 /*ALL*/ ? p.n : (long long)p.n_seeds;
+  } else {
+    ncand = c.ncand;
+    Kreq = c.K_next;
+  }
+  long long K = Kreq < ncand ? Kreq : ncand;
+  if (K > p.S_cap) { c.status = 5 /*CAPACITY*/; c.phase = PH_ERROR; return; }
+  c.K_r = (int)K;
+  c.sample_count = 0;
+  c.kth = ~0ull;
+  if (K >= ncand) {
+    c.take_all = 1;
+    c.thresh = ~0ull;
+  } else {
+    c.take_all = 0;
+    double frac = ((double)K + 4.0 * sqrt((double)K) + 64.0) / (double)ncand;
+    c.thresh = frac >= 1.0 ? ~0ull : (unsigned long long)(frac * 18446744073709551616.0);
+  }
+}
+
+__global__ void sel_collect_kernel(Params p) {
+  const int f = blockIdx.y;
+  FrameCtl& c = p.ctl[f];
+  if (c.phase != PH_SELECT || c.take_all) return;
+  const int round = c.round;
+  const unsigned long long T = c.thresh;
+  const int lane = threadIdx.x & 31;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < p.n; i0 += (long long)gridDim.x * blockDim.x) {
+    const long long i = i0 + threadIdx.x;
+    bool take = false;
+    unsigned long long key = 0;
+    if (i < p.n && is_candidate(p, f, round, i)) {
+      key = sel_key(p.rng_seed, round, i);
+      take = key < T;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (m) {
+      long long base = 0;
+      if (lane == 0) base = (long long)atomicAdd((unsigned long long*)&c.sample_count, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (take) {
+        long long pos = base + __popc(m & ((1u << lane) - 1));
+        if (pos < p.sample_cap) p.sample[(size_t)f * p.sample_cap + pos] = key;
+      }
+    }
+  }
+}
+
+// K-th smallest (1-based) key by MSD radix select, 8 bits per pass.  from_sample selects the key
+// source: the sample buffer, or (fallback) every candidate pixel recomputed on the fly.
+__device__ unsigned long long radix_kth(const Params& p, int f, int round, bool from_sample, long long count,
+                                        long long k) {
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ long long s_k;
+  if (threadIdx.x == 0) { s_prefix = 0; s_k = k; }
+  unsigned long long mask = 0;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const unsigned long long prefix = s_prefix;
+    for (long long idx = threadIdx.x; idx < count; idx += blockDim.x) {
+      unsigned long long key;
+      if (from_sample) {
+        key = p.sample[(size_t)f * p.sample_cap + idx];
+      } else {
+        if (!is_candidate(p, f, round, idx)) continue;
+        key = sel_key(p.rng_seed, round, idx);
+      }
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long cum = 0;
+      for (int b = 0; b < 256; ++b) {
+        if (cum + hist[b] >= s_k) {
+          s_prefix |= (unsigned long long)b << shift;
+          s_k -= cum;
+          break;
+        }
+        cum += hist[b];
+      }
+    }
+    mask |= 0xFFull << shift;
+    __syncthreads();
+  }
+  return s_prefix;
+}
+
+__global__ void sel_kth_kernel(Params p) {
+  const int f = blockIdx.x;
+  FrameCtl& c = p.ctl[f];
+  if (c.phase != PH_SELECT || c.take_all) return;
+  const long long M = c.sample_count;
+  const long long K = c.K_r;
+  unsigned long long kth;
+  if (M >= K && M <= p.sample_cap) {
+    kth = radix_kth(p, f, c.round, true, M, K);
+  } else {
+    kth = radix_kth(p, f, c.round, false, p.n, K);  // rare: sample too small / overflowed
+  }
+  if (threadIdx.x == 0) c.kth = kth;
+}
+
+constexpr int kSelBlock = 2048;  // pixels per block in count/write (256 threads x 8)
+
+__device__ __forceinline__ bool is_selected(const Params& p, int f, const FrameCtl& c, long long i) {
+  if (!is_candidate(p, f, c.round, i)) return false;
+  if (c.take_all) return true;
+  return sel_key(p.rng_seed, c.round, i) <= c.kth;
+}
+
+__global__ void sel_count_kernel(Params p) {
+  const int f = blockIdx.y;
+  const FrameCtl& c = p.ctl[f];
+  if (c.phase != PH_SELECT) return;
+  const long long base = (long long)blockIdx.x * kSelBlock;
+  int cnt = 0;
+  for (int u = 0; u < kSelBlock / 256; ++u) {
+    long long i = base + u * 256 + threadIdx.x;
+    if (i < p.n && is_selected(p, f, c, i)) ++cnt;
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  __shared__ int ws[8];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < 8; ++w) s += ws[w];
+    p.blkcnt[(size_t)f * p.nblk + blockIdx.x] = s;
+  }
+}
+
+__global__ void sel_scan_kernel(Params p) {
+  const int f = blockIdx.x;
+  FrameCtl& c = p.ctl[f];
+  if (c.phase != PH_SELECT) return;
+  __shared__ int sm[33];
+  int carry = 0;
+  for (int b0 = 0; b0 < p.nblk; b0 += blockDim.x) {
+    int b = b0 + threadIdx.x;
+    int v = b < p.nblk ? p.blkcnt[(size_t)f * p.nblk + b] : 0;
+    int tot;
+    int ex = block_excl_scan(v, sm, &tot);
+    if (b < p.nblk) p.blkcnt[(size_t)f * p.nblk + b] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && carry != c.K_r) {
+    c.status = 9;  // internal: selection count mismatch
+    c.phase = PH_ERROR;
+  }
+}
+
+template <int DP>
+__global__ void sel_write_kernel(Params p) {
+  const int f = blockIdx.y;
+  const FrameCtl& c = p.ctl[f];
+  if (c.phase != PH_SELECT) return;
+  __shared__ int sm[33];
+  const long long base = (long long)blockIdx.x * kSelBlock + (long long)threadIdx.x * 8;
+  unsigned sel = 0;
+  for (int u = 0; u < 8; ++u) {
+    long long i = base + u;
+    if (i < p.n && is_selected(p, f, c, i)) sel |= 1u << u;
+  }
+  int pos = p.blkcnt[(size_t)f * p.nblk + blockIdx.x] + block_excl_scan(__popc(sel), sm, nullptr);
+  for (int u = 0; u < 8; ++u) {
+    if (!(sel & (1u << u))) continue;
+    const long long i = base + u;
+    const size_t so = (size_t)f * p.S_cap + pos;
+    const float inv = p.inv[(size_t)f * p.n + i];
+    const float* x = p.emb + ((size_t)f * p.n + i) * p.d;
+    float* s = p.seeds + so * DP;
+    __half* sh = p.sop + ((size_t)f * p.S_pad + pos) * DP;
+#pragma unroll
+    for (int k = 0; k < DP; ++k) {
+      float v = k < p.d ? x[k] * inv : 0.f;
+      s[k] = v;
+      sh[k] = __float2half_rn(v);
+    }
+    p.sorig[so] = (int)i;
+    p.sstat[so] = ST_ACTIVE;
+    p.scnt[so] = 0;
+    p.act[so] = pos;
+    p.flags[(size_t)f * p.n + i] |= PF_VISITED;
+    ++pos;
+  }
+}
+
+__global__ void sel_finish_kernel(Params p) {
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= p.B) return;
+  FrameCtl& c = p.ctl[f];
+  if (c.phase != PH_SELECT) return;
+  const int K = c.K_r;
+  c.phase = PH_ITERATE;
+  c.t = 0;
+  c.n_active = K;
+  c.n_conv = 0;
+  const double g = p.kind == 2 ? 1.0 : p.gamma;
+  double need = ceil(g * (double)K - 1e-9);
+  c.need = need < 0 ? 0 : (int)need;
+  c.total += K;
+  c.round_K[c.round] = K;
+  c.round_seed_iters[c.round] = 0;
+  // split-pixel factor: fixed for the round, from the frame's own K_r (independent of batching)
+  const int tiles = (K + kBM - 1) / kBM;
+  int splits = kItemTarget / (tiles > 0 ? tiles : 1);
+  if (splits < 1) splits = 1;
+  if (splits > p.n_ptiles) splits = p.n_ptiles;
+  c.chunk_tiles = (p.n_ptiles + splits - 1) / splits;
+  c.splits = (p.n_ptiles + c.chunk_tiles - 1) / c.chunk_tiles;
+  if (K == 0) { c.phase = PH_POST; }
+}
+
+// ------------------------------------------------------------------------------------------------
+cudaError_t launch_prep(const Params& p, cudaStream_t st) {
+  init_ctl_kernel<<<(p.B + 127) / 128, 128, 0, st>>>(p);
+  dim3 g((unsigned)((p.n_pad + 255) / 256), p.B);
+  if (p.DP == 16) prep_kernel<16><<<g, 256, 0, st>>>(p);
+  else prep_kernel<32><<<g, 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select(const Params& p, int num_sms, cudaStream_t st) {
+  sel_prepare_kernel<<<(p.B + 127) / 128, 128, 0, st>>>(p);
+  int gx = (int)((p.n + 255) / 256);
+  int cap = (num_sms * 8 + p.B - 1) / p.B;
+  if (gx > cap) gx = cap;
+  if (gx < 1) gx = 1;
+  sel_collect_kernel<<<dim3(gx, p.B), 256, 0, st>>>(p);
+  sel_kth_kernel<<<p.B, 1024, 0, st>>>(p);
+  sel_count_kernel<<<dim3(p.nblk, p.B), 256, 0, st>>>(p);
+  sel_scan_kernel<<<p.B, 1024, 0, st>>>(p);
+  if (p.DP == 16) sel_write_kernel<16><<<dim3(p.nblk, p.B), 256, 0, st>>>(p);
+  else sel_write_kernel<32><<<dim3(p.nblk, p.B), 256, 0, st>>>(p);
+  sel_finish_kernel<<<(p.B + 127) / 128, 128, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace fms

@@ -1,0 +1,476 @@
+// runtime.cu -- host runtime behind the C ABI (include/fms.h): context, workspace, TMA descriptors
+// and the device-resident OSOP round/step loop.
+//
+// Control flow for a batch of B frames (every frame owns an independent FrameCtl state machine;
+// the host only launches kernels and polls one small counter block):
+//
+//   init + K1 prep
+//   repeat (rounds):                                   OSOP round
+//     K6 select (7 small kernels; frames in SELECT)      Alg. 2 l.2
+//     repeat (lockstep steps, polled every kPoll):       Alg. 2 l.4-9
+//       plan -> K2 iter (tcgen05) -> K3 update -> ctl_step
+//     K4 merge -> K5 assign -> K7 osop                   P:223, Eq. 19
+//   output centres
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fms.h"
+#include "fms_device.cuh"
+
+namespace fms {
+cudaError_t launch_prep(const Params& p, cudaStream_t st);
+cudaError_t launch_select(const Params& p, int num_sms, cudaStream_t st);
+cudaError_t launch_plan(const Params& p, cudaStream_t st);
+cudaError_t launch_iter(int DP, const CUtensorMap& tx, const CUtensorMap& ts, const Params& p, int grid,
+                        cudaStream_t st);
+cudaError_t launch_update_ctl(const Params& p, int num_sms, cudaStream_t st);
+cudaError_t launch_post(const Params& p, cudaStream_t st);
+cudaError_t launch_output(const Params& p, float* centres_out, int cap, cudaStream_t st);
+cudaError_t setup_iter_attrs();
+cudaError_t setup_post_attrs(int P_cap);
+}  // namespace fms
+
+using namespace fms;
+
+namespace {
+
+constexpr int kPoll = 4;            // lockstep steps launched between host polls
+constexpr int kMaxPcap = 16384;     // merge pool capacity (SMEM bitonic sort)
+constexpr int kCounters = 64;
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  std::string err;
+  bool profile = false;
+  bool attrs_done = false;
+  // device workspace (one allocation, carved per call)
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  // staging for the host-pointer entry point
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  // pinned host scratch
+  int* h_counters = nullptr;
+  FrameCtl* h_ctl = nullptr;
+  size_t h_ctl_cap = 0;
+  // profiling
+  std::vector<cudaEvent_t> ev;
+  int* h_prof = nullptr;   // per launch: counters[0..7] snapshot
+  size_t h_prof_cap = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+};
+
+fms_status fail(Ctx* c, fms_status s, const std::string& m) {
+  if (c) c->err = m;
+  return s;
+}
+
+#define CU(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t _e = (call);                                                                      \
+    if (_e != cudaSuccess)                                                                        \
+      return fail(c, FMS_E_CUDA, std::string(#call " failed: ") + cudaGetErrorString(_e));       \
+  } while (0)
+
+fms_status make_tmap(Ctx* c, CUtensorMap* m, void* base, uint64_t rows, int DP) {
+  if (!c->encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    CU(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(c, FMS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    c->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)DP, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)DP * 2};
+  cuuint32_t box[2] = {(cuuint32_t)DP, (cuuint32_t)kBN};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = c->encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, base, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         DP == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, FMS_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return FMS_OK;
+}
+
+fms_status validate(Ctx* c, int32_t B, int64_t n, int32_t d, double h, int32_t max_iters, double tol,
+                    const fms_seed_policy* pol) {
+  if (!c) return FMS_E_INVALID;
+  if (B < 1 || n < 1 || d < 1 || d > 32) return fail(c, FMS_E_INVALID, "need B>=1, n>=1, 1<=d<=32");
+  if (!(h > 0.0 && h < 1.0)) return fail(c, FMS_E_INVALID, "bandwidth must be in (0,1) (cosine distance)");
+  if (!(tol > 0.0) || max_iters < 1) return fail(c, FMS_E_INVALID, "need tol>0 and max_iters>=1");
+  if (!pol) return fail(c, FMS_E_INVALID, "policy is NULL");
+  if (pol->kind < 0 || pol->kind > 2) return fail(c, FMS_E_INVALID, "bad policy kind");
+  if (pol->kind != FMS_SEEDS_ALL && pol->n_seeds < 1) return fail(c, FMS_E_INVALID, "n_seeds must be >= 1");
+  if (!(pol->gamma > 0.0 && pol->gamma <= 1.0)) return fail(c, FMS_E_INVALID, "gamma must be in (0,1]");
+  if (pol->max_rounds < 1 || pol->max_rounds > FMS_MAX_ROUNDS) return fail(c, FMS_E_INVALID, "max_rounds in 1..16");
+  if (pol->kind == FMS_SEEDS_OSOP && (!(pol->P > 0.0 && pol->P < 1.0) || !(pol->L > 0.0)))
+    return fail(c, FMS_E_INVALID, "OSOP needs 0<P<1 and L>0");
+  if ((double)B * (double)align_up((size_t)n, kBN) >= 2147483647.0)
+    return fail(c, FMS_E_INVALID, "B*n too large for 32-bit TMA coordinates");
+  return FMS_OK;
+}
+
+// carve the workspace; returns required bytes (and fills pointers if base != nullptr)
+size_t carve(Params& p, uint8_t* base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> void* {
+    off = align_up(off, 1024);
+    void* r = base ? base + off : nullptr;
+    off += bytes;
+    return r;
+  };
+  const size_t B = p.B;
+  p.Xh = (__half*)take(B * p.n_pad * p.DP * 2);
+  p.inv = (float*)take(B * p.n * 4);
+  p.flags = (uint8_t*)take(B * p.n);
+  p.seeds = (float*)take(B * (size_t)p.S_cap * p.DP * 4);
+  p.sop = (__half*)take(B * (size_t)p.S_pad * p.DP * 2);
+  p.sorig = (int*)take(B * (size_t)p.S_cap * 4);
+  p.sstat = (uint8_t*)take(B * (size_t)p.S_cap);
+  p.scnt = (int*)take(B * (size_t)p.S_cap * 4);
+  p.act = (int*)take(B * (size_t)p.S_cap * 4);
+  p.cent = (float*)take(B * (size_t)p.C_cap * p.DP * 4);
+  p.cint = (int*)take(B * (size_t)p.C_cap * 4);
+  p.corig = (int*)take(B * (size_t)p.C_cap * 4);
+  p.hist = (int*)take(B * (size_t)p.C_cap * 4);
+  p.pool = (float*)take(B * (size_t)p.P_cap * p.DP * 4);
+  p.pint = (int*)take(B * (size_t)p.P_cap * 4);
+  p.porg = (int*)take(B * (size_t)p.P_cap * 4);
+  p.part_g = (float*)take((size_t)p.items_cap * kBM * p.DP * 4);
+  p.part_c = (int*)take((size_t)p.items_cap * kBM * 4);
+  p.items = (WorkItem*)take((size_t)p.items_cap * sizeof(WorkItem));
+  p.tiles = (TileTask*)take((size_t)p.tiles_cap * sizeof(TileTask));
+  p.counters = (int*)take(kCounters * 4);
+  p.sample = (unsigned long long*)take(B * (size_t)p.sample_cap * 8);
+  p.blkcnt = (int*)take(B * (size_t)p.nblk * 4);
+  p.ctl = (FrameCtl*)take(B * sizeof(FrameCtl));
+  return align_up(off, 1024);
+}
+
+fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, double h, int32_t max_iters,
+                     double tol, const fms_seed_policy* pol, int32_t* labels, float* centres, int32_t cap,
+                     int32_t* K_out, fms_frame_stats* fs, fms_run_stats* rs, cudaStream_t st) {
+  fms_status v = validate(c, B, n, d, h, max_iters, tol, pol);
+  if (v != FMS_OK) return v;
+  if (!emb || !labels || !K_out || (cap > 0 && !centres) || cap < 0) return fail(c, FMS_E_INVALID, "null buffer");
+  CU(cudaSetDevice(c->device));
+  if (!c->attrs_done) {
+    CU(setup_iter_attrs());
+    CU(setup_post_attrs(kMaxPcap));
+    CU(cudaEventCreate(&c->t0));
+    CU(cudaEventCreate(&c->t1));
+    c->attrs_done = true;
+  }
+  Params p{};
+  p.B = B;
+  p.d = d;
+  p.DP = d <= 16 ? 16 : 32;
+  p.max_iter = max_iters;
+  p.n = n;
+  p.n_pad = (long long)align_up((size_t)n, kBN);
+  p.n_ptiles = (int)(p.n_pad / kBN);
+  long long S = pol->kind == FMS_SEEDS_FIXED ? std::min<long long>(pol->n_seeds, n) : n;
+  p.S_cap = (int)S;
+  p.S_pad = (int)align_up((size_t)S, kBM);
+  p.C_cap = (int)std::min<long long>(n, 65536);
+  p.P_cap = (int)std::min<long long>((long long)p.C_cap + p.S_cap, kMaxPcap);
+  p.tiles_cap = B * (p.S_pad / kBM);
+  p.items_cap = B * std::max(kItemTarget, p.S_pad / kBM);
+  p.sample_cap = (int)std::min<long long>(n, (long long)S + 8 * (long long)std::sqrt((double)S) + 1024);
+  p.nblk = (int)((n + 2047) / 2048);
+  p.h = h;
+  p.tau = 1.0 - h;
+  p.tau_f = (float)(1.0 - h);
+  p.rho_f = (float)(1.0 - h);  // merge radius rho = h (R10): keep unless x.c >= 1 - rho
+  p.tol = tol;
+  p.kind = pol->kind;
+  p.n_seeds = pol->n_seeds;
+  p.has_bg = pol->has_background;
+  p.min_px = pol->min_instance_px;
+  p.sat_stop = pol->saturation_stop;
+  p.max_rounds = pol->max_rounds;
+  p.gamma = pol->gamma;
+  p.L = pol->L;
+  p.H = pol->H;
+  p.P = pol->P;
+  p.rng_seed = pol->rng_seed;
+  p.emb = emb;
+  p.labels = labels;
+
+  const size_t need = carve(p, nullptr);
+  if (need > c->ws_bytes) {
+    if (c->ws) cudaFree(c->ws);
+    c->ws = nullptr;
+    c->ws_bytes = 0;
+    if (cudaMalloc(&c->ws, need) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, FMS_E_OOM, "workspace allocation of " + std::to_string(need) + " bytes failed");
+    }
+    c->ws_bytes = need;
+  }
+  carve(p, reinterpret_cast<uint8_t*>(c->ws));
+  if ((size_t)B > c->h_ctl_cap) {
+    if (c->h_ctl) cudaFreeHost(c->h_ctl);
+    CU(cudaMallocHost(&c->h_ctl, sizeof(FrameCtl) * B));
+    c->h_ctl_cap = B;
+  }
+  if (!c->h_counters) CU(cudaMallocHost(&c->h_counters, kCounters * 4));
+
+  CUtensorMap tmx, tms;
+  fms_status ts = make_tmap(c, &tmx, p.Xh, (uint64_t)B * p.n_pad, p.DP);
+  if (ts != FMS_OK) return ts;
+  ts = make_tmap(c, &tms, p.sop, (uint64_t)B * p.S_pad, p.DP);
+  if (ts != FMS_OK) return ts;
+
+  CU(cudaEventRecord(c->t0, st));
+  CU(cudaMemsetAsync(p.counters, 0, kCounters * 4, st));
+  CU(launch_prep(p, st));
+  int steps = 0, launches = 0;
+  std::vector<int> prof_slots;
+  for (int round = 0; round < pol->max_rounds + 1; ++round) {
+    CU(launch_select(p, c->num_sms, st));
+    for (int s = 0; s < max_iters + kPoll; s += kPoll) {
+      for (int k = 0; k < kPoll; ++k) {
+        CU(launch_plan(p, st));
+        if (c->profile) {
+          const size_t slot = launches;
+          if (c->ev.size() < 2 * (slot + 1)) {
+            cudaEvent_t e0, e1;
+            CU(cudaEventCreate(&e0));
+            CU(cudaEventCreate(&e1));
+            c->ev.push_back(e0);
+            c->ev.push_back(e1);
+          }
+          if (c->h_prof_cap < slot + 1) {
+            size_t ncap = std::max<size_t>(256, 2 * (slot + 1));
+            int* np = nullptr;
+            CU(cudaMallocHost(&np, ncap * 8 * sizeof(int)));
+            if (c->h_prof) {
+              CU(cudaStreamSynchronize(st));
+              memcpy(np, c->h_prof, c->h_prof_cap * 8 * sizeof(int));
+              cudaFreeHost(c->h_prof);
+            }
+            c->h_prof = np;
+            c->h_prof_cap = ncap;
+          }
+          CU(cudaEventRecord(c->ev[2 * slot], st));
+          CU(launch_iter(p.DP, tmx, tms, p, c->num_sms, st));
+          CU(cudaEventRecord(c->ev[2 * slot + 1], st));
+          CU(cudaMemcpyAsync(c->h_prof + slot * 8, p.counters, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+          ++launches;
+        } else {
+          CU(launch_iter(p.DP, tmx, tms, p, c->num_sms, st));
+        }
+        CU(launch_update_ctl(p, c->num_sms, st));
+        ++steps;
+      }
+      CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      if (c->h_counters[5]) return fail(c, FMS_E_INTERNAL, "work-item capacity exceeded");
+      if (c->h_counters[3] == 0) break;  // no frame still iterating
+    }
+    CU(launch_post(p, st));
+    CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (c->h_counters[2] == 0) break;  // every frame DONE (or in error)
+  }
+  if (cap > 0) CU(launch_output(p, centres, cap, st));
+  CU(cudaEventRecord(c->t1, st));
+  CU(cudaMemcpyAsync(c->h_ctl, p.ctl, sizeof(FrameCtl) * B, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  CU(cudaGetLastError());
+
+  fms_status result = FMS_OK;
+  for (int f = 0; f < B; ++f) {
+    const FrameCtl& fc = c->h_ctl[f];
+    K_out[f] = fc.Kc;
+    fms_status s = FMS_OK;
+    if (fc.status != 0) s = (fms_status)fc.status;
+    else if (fc.phase != PH_DONE) s = FMS_E_INTERNAL;
+    else if (fc.Kc > cap) s = FMS_E_CAPACITY;
+    if (s != FMS_OK && result == FMS_OK) {
+      result = s;
+      c->err = "frame " + std::to_string(f) + " status " + std::to_string((int)s);
+    }
+    if (fs) {
+      fms_frame_stats& o = fs[f];
+      memset(&o, 0, sizeof(o));
+      o.status = s;
+      o.rounds = std::min(fc.round + 1, FMS_MAX_ROUNDS);
+      o.K = fc.Kc;
+      o.seeds_total = fc.total;
+      o.seed_iters = fc.seed_iters;
+      long long disc = 0;
+      for (int r = 0; r < o.rounds; ++r) {
+        o.round_K[r] = fc.round_K[r];
+        o.round_iters[r] = fc.round_iters[r];
+        o.round_conv[r] = fc.round_conv[r];
+        o.round_disc[r] = fc.round_disc[r];
+        o.round_Kc[r] = fc.round_Kc[r];
+        o.round_I[r] = fc.round_I[r];
+        o.round_seed_iters[r] = fc.round_seed_iters[r];
+        o.round_cand[r] = fc.round_cand[r];
+        o.round_r[r] = fc.round_r[r];
+        o.round_nmin[r] = fc.round_nmin[r];
+        disc += fc.round_disc[r];
+      }
+      o.discarded = disc;
+    }
+  }
+  if (rs) {
+    memset(rs, 0, sizeof(*rs));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->t0, c->t1);
+    rs->ms_total = ms;
+    rs->workspace_bytes = (int64_t)c->ws_bytes;
+    rs->steps = steps;
+    if (c->profile) {
+      for (int l = 0; l < launches; ++l) {
+        const int* snap = c->h_prof + (size_t)l * 8;
+        if (snap[0] <= 0) continue;
+        float t = 0.f;
+        cudaEventElapsedTime(&t, c->ev[2 * l], c->ev[2 * l + 1]);
+        rs->iter_ms += t;
+        rs->iter_launches += 1;
+        rs->iter_items += snap[0];
+        rs->iter_seed_iters += reinterpret_cast<const long long*>(snap + 6)[0];
+      }
+    }
+  }
+  return result;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fms_version(void) { return "fms-b200 0.1 (sm_100a, tcgen05)"; }
+
+fms_status fms_default_policy(fms_seed_policy* o) {
+  if (!o) return FMS_E_INVALID;
+  memset(o, 0, sizeof(*o));
+  o->kind = FMS_SEEDS_OSOP;
+  o->n_seeds = 128;
+  o->gamma = 0.9;
+  o->L = 2.0;
+  o->H = 8.0;
+  o->P = 0.99;
+  o->has_background = 1;
+  o->max_rounds = 8;
+  return FMS_OK;
+}
+
+fms_status fms_ctx_create(void** out, int device) {
+  if (!out) return FMS_E_INVALID;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return FMS_E_CUDA;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return FMS_E_CUDA;
+  if (prop.major != 10) return FMS_E_CUDA;  // sm_100a build
+  Ctx* c = new Ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  *out = c;
+  return FMS_OK;
+}
+
+void fms_ctx_destroy(void* ctx) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->ws) cudaFree(c->ws);
+  if (c->stage) cudaFree(c->stage);
+  if (c->h_counters) cudaFreeHost(c->h_counters);
+  if (c->h_ctl) cudaFreeHost(c->h_ctl);
+  if (c->h_prof) cudaFreeHost(c->h_prof);
+  for (auto e : c->ev) cudaEventDestroy(e);
+  if (c->t0) cudaEventDestroy(c->t0);
+  if (c->t1) cudaEventDestroy(c->t1);
+  delete c;
+}
+
+const char* fms_last_error(const void* ctx) {
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  return c ? c->err.c_str() : "null context";
+}
+
+fms_status fms_set_option(void* ctx, const char* key, int64_t value) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !key) return FMS_E_INVALID;
+  if (!strcmp(key, "profile_iter")) {
+    c->profile = value != 0;
+    return FMS_OK;
+  }
+  return fail(c, FMS_E_INVALID, std::string("unknown option ") + key);
+}
+
+fms_status fms_cluster_batch(void* ctx, const float* emb, int32_t B, int64_t n, int32_t d, double bandwidth,
+                             int32_t max_iters, double tol, const fms_seed_policy* policy, int32_t* labels,
+                             float* centres, int32_t centres_cap, int32_t* K_out, fms_frame_stats* frame_stats,
+                             fms_run_stats* run_stats, void* stream) {
+  return run_batch(static_cast<Ctx*>(ctx), emb, B, n, d, bandwidth, max_iters, tol, policy, labels, centres,
+                   centres_cap, K_out, frame_stats, run_stats, static_cast<cudaStream_t>(stream));
+}
+
+fms_status fms_cluster(void* ctx, const float* emb, int64_t n, int32_t d, double bandwidth, int32_t max_iters,
+                       double tol, const fms_seed_policy* policy, int32_t* labels, float* centres,
+                       int32_t centres_cap, int32_t* K_out, fms_frame_stats* frame_stats,
+                       fms_run_stats* run_stats, void* stream) {
+  return fms_cluster_batch(ctx, emb, 1, n, d, bandwidth, max_iters, tol, policy, labels, centres, centres_cap,
+                           K_out, frame_stats, run_stats, stream);
+}
+
+fms_status fms_cluster_batch_host(void* ctx, const float* emb_host, int32_t B, int64_t n, int32_t d,
+                                  double bandwidth, int32_t max_iters, double tol,
+                                  const fms_seed_policy* policy, int32_t* labels_host, float* centres_host,
+                                  int32_t centres_cap, int32_t* K_out, fms_frame_stats* frame_stats,
+                                  fms_run_stats* run_stats, void* stream) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  fms_status v = validate(c, B, n, d, bandwidth, max_iters, tol, policy);
+  if (v != FMS_OK) return v;
+  if (!emb_host || !labels_host || !K_out || centres_cap < 0 || (centres_cap > 0 && !centres_host))
+    return fail(c, FMS_E_INVALID, "null buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CU(cudaSetDevice(c->device));
+  const size_t eb = align_up((size_t)B * n * d * 4, 1024);
+  const size_t lb = align_up((size_t)B * n * 4, 1024);
+  const size_t cb = align_up((size_t)B * std::max(centres_cap, 1) * d * 4, 1024);
+  if (eb + lb + cb > c->stage_bytes) {
+    if (c->stage) cudaFree(c->stage);
+    c->stage = nullptr;
+    c->stage_bytes = 0;
+    if (cudaMalloc(&c->stage, eb + lb + cb) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, FMS_E_OOM, "staging allocation failed");
+    }
+    c->stage_bytes = eb + lb + cb;
+  }
+  float* d_emb = reinterpret_cast<float*>(c->stage);
+  int32_t* d_lab = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(c->stage) + eb);
+  float* d_cen = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(c->stage) + eb + lb);
+  CU(cudaMemcpyAsync(d_emb, emb_host, (size_t)B * n * d * 4, cudaMemcpyHostToDevice, st));
+  fms_status s = run_batch(c, d_emb, B, n, d, bandwidth, max_iters, tol, policy, d_lab, d_cen, centres_cap, K_out,
+                           frame_stats, run_stats, st);
+  if (s != FMS_OK && s != FMS_E_CAPACITY) return s;
+  CU(cudaMemcpyAsync(labels_host, d_lab, (size_t)B * n * 4, cudaMemcpyDeviceToHost, st));
+  if (centres_cap > 0)
+    CU(cudaMemcpyAsync(centres_host, d_cen, (size_t)B * centres_cap * d * 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return s;
+}
+
+}  // extern "C"
