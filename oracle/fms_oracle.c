@@ -152,7 +152,8 @@ int64_t fmso_window(const double* xhat, int64_t n, int32_t d, double tau, const 
  *     converged if |s' - s|_2 < tol             (R6: "change ... less than ... h/1,000")
  * Converged seeds freeze (R9).  The batch stops once converged >= ceil(gamma*K) (R8) or no seed is
  * active; seeds still moving are "discarded from the seed vector".  An empty window
- * (impossible for seeds started at data points, pin P3) marks the seed stalled.
+ * (impossible for seeds started at data points, pin P3) marks the seed stalled.  Each converged
+ * mode gets its intensity = |S_h(m)| (density of Eq. 2 at the mode, R10).
  * ------------------------------------------------------------------------------------------- */
 int32_t fmso_lockstep(const double* xhat, int64_t n, int32_t d, double h, int32_t max_iter,
                       double tol, double gamma, int64_t K, double* seeds, uint8_t* status,
@@ -184,7 +185,6 @@ int32_t fmso_lockstep(const double* xhat, int64_t n, int32_t d, double h, int32_
         dd += (sn[k] - s[k]) * (sn[k] - s[k]);
       }
       for (int32_t k = 0; k < d; ++k) s[k] = sn[k];
-      intensity[j] = cnt;
       iters[j] = t;
       if (sqrt(dd) < tol) status[j] = 1;
     }
@@ -194,6 +194,14 @@ int32_t fmso_lockstep(const double* xhat, int64_t n, int32_t d, double h, int32_
   }
   for (int64_t j = 0; j < K; ++j)
     if (status[j] == 0) status[j] = 3;
+  /* intensity of a converged mode m (R10): the flat-kernel density of Eq. 2 at m up to the constant
+   * 1/(n h^d), i.e. the number of points in the window centred on m. */
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t j = 0; j < K; ++j) {
+    if (status[j] != 1) continue;
+    double g[256];
+    intensity[j] = fmso_window(xhat, n, d, tau, seeds + j * d, g);
+  }
   return t_run;
 }
 

@@ -62,8 +62,8 @@ int64_t fmso_select(const uint8_t* cand, int64_t n, int64_t K, uint64_t rng_seed
 int64_t fmso_window(const double* xhat, int64_t n, int32_t d, double tau,
                     const double* s, double* g);                                  /* Eq. 8+11 */
 /* Lockstep mean-shift over K seeds (Alg. 2 l.4-9 + early stop).  seeds[K*d] in/out, status[K]:
- * 1 converged, 2 stalled, 3 discarded.  Returns iterations run; writes intensity (window count of
- * the final update, R10) and per-seed iteration count. */
+ * 1 converged, 2 stalled, 3 discarded.  Returns iterations run; writes, for converged seeds, the
+ * intensity |S_h(m)| (flat-kernel density of Eq. 2 at the mode, R10) and per-seed iterations. */
 int32_t fmso_lockstep(const double* xhat, int64_t n, int32_t d, double h, int32_t max_iter,
                       double tol, double gamma, int64_t K, double* seeds, uint8_t* status,
                       int64_t* intensity, int32_t* iters, int64_t* seed_iters);

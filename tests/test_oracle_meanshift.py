@@ -186,6 +186,14 @@ def test_early_stop_bound_and_status():
     for m in out["seeds"][st == 1]:
         g, _ = oracle.window(X, m, 0.1)
         assert np.linalg.norm(g / np.linalg.norm(g) - m) < 1e-4
+    # intensity of a mode = number of points in its window (Eq. 2 density at the mode, R10),
+    # pinned to sklearn's radius query (|x - m| <= sqrt(2h) for unit vectors)
+    nn = NearestNeighbors(radius=np.sqrt(2 * 0.1)).fit(X)
+    modes = out["seeds"][st == 1]
+    got = out["intensity"][st == 1]
+    want = np.array([len(r) for r in nn.radius_neighbors(modes, return_distance=False)])
+    band = np.array([np.any(np.abs(X @ m - 0.9) < 1e-12) for m in modes])
+    assert np.array_equal(got[~band], want[~band])
 
 
 # --------------------------------------------------------------------------------------------
