@@ -1,0 +1,295 @@
+"""Benchmark of the Faster Mean-shift hot path on B200 (one JSON line on rank 0).
+
+metric: frames/sec clustering 512x512 frames of 16-D embeddings (BASELINE.json configs[1], the
+        metric config: ~30 touching/overlapping cells, full OSOP), plus the iteration kernel's
+        fraction of its tensor roofline.
+step  : one call of fms_cluster_batch on a batch of B resident frames (every §8(a) row runs:
+        normalise, select, lockstep iteration, intensity, merge, assign, OSOP control).
+multi-GPU: frames are independent (replicas, no data-path collective); each rank
+        clusters its own batches; the elapsed time is the max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl fms|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = "C2"
+H = 0.1
+MAX_ITERS = 300
+CAP = 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--impl", default="fms", choices=["fms", "reference"])
+    ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def policy_kwargs(n):
+    from synth.frames import min_instance_px
+    return dict(min_instance_px=min_instance_px(n), saturation_stop=1)
+
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "fms":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl")
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, local
+
+
+class ClockSampler:
+    """SM clocks and throttle reasons sampled (NVML, every 50 ms) during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.err = None
+
+    def _run(self):
+        import pynvml
+        try:
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self.stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                util = pynvml.nvmlDeviceGetUtilizationRates(h).gpu
+                self.rows.append((sm, mx, rs, util))
+                self.stop.wait(0.05)
+        except Exception as e:  # pragma: no cover
+            self.err = repr(e)
+
+    def __enter__(self):
+        import threading
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=5)
+
+    def summary(self):
+        rows = [r for r in self.rows if r[3] > 0] or self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err}
+        sm = sorted(r[0] for r in rows)
+        reasons = sorted({name for r in rows for bit, name in self.REASONS.items() if r[2] & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return m, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per K2 launch from the committed ncu --set full summary, if present."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "iter_kernel_ncu.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(frames, budget_s=20.0):
+    """The oracle as it stands, on a bounded sample of the same workload (rank 0, N=1 only)."""
+    import oracle
+    pk = policy_kwargs(frames[0].n)
+    done, t0 = 0, time.perf_counter()
+    for f in frames:
+        r = oracle.cluster(f.emb, h=H, max_iter=MAX_ITERS, pol=oracle.policy(rng_seed=f.seed, **pk))
+        assert r.status == 0
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "frames/s", "cores": oracle.lib().fmso_num_threads(), "kind": "oracle",
+            "sample": f"{done} {frames[0].config} frame(s) ({frames[0].H}x{frames[0].W}x{frames[0].D}), "
+                      f"fp64 C oracle with OpenMP, {dt:.1f} s"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    import synth
+    frames = [synth.make_frame(args.config, 1000 + i) for i in range(max(1, args.steps + args.warmup))]
+    for f in frames[:args.warmup]:
+        cpu_baseline([f], budget_s=0)
+    t0 = time.perf_counter()
+    cb = cpu_baseline(frames[args.warmup:args.warmup + args.steps], budget_s=1e9)
+    dt = time.perf_counter() - t0
+    f0 = frames[0]
+    line = {"impl": "reference", "metric": f"frames/sec ({f0.H}x{f0.W}, {f0.D}-D embeddings)",
+            "value": cb["value"], "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3 / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {f0.H}x{f0.W} frame, {f0.D}-D, {f0.cells} cells + background, "
+                                   "full OSOP", "frames_per_step": 1},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    import numpy as np
+    import torch
+
+    import paper_2007_14283_b200 as fms
+    import synth
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    B = args.batch
+    # pool of 2 batches (inputs 2 x B x 16 MiB > 126 MB L2 for B >= 4), alternated step to step
+    frames = [synth.make_frame(args.config, 10000 * rank + i) for i in range(2 * B)]
+    n, d = frames[0].n, frames[0].D
+    pool = torch.from_numpy(np.stack([f.emb for f in frames])).to(dev).view(2, B, n, d)
+    labels = torch.empty((B, n), dtype=torch.int32, device=dev)
+    cent = torch.empty((B, CAP, d), dtype=torch.float32, device=dev)
+    ctx = fms.context(local)
+    pol = fms.default_policy(**policy_kwargs(n))
+    stream = torch.cuda.current_stream(dev)
+
+    def step(k, profile=False):
+        rc, K, fs, rs = ctx.cluster_batch_ptr(pool[k % 2].data_ptr(), B, n, d, labels.data_ptr(), cent.data_ptr(),
+                                              CAP, H, MAX_ITERS, None, pol, stream.cuda_stream)
+        return fs, rs
+
+    for k in range(args.warmup):
+        step(k)
+    ctx.set_option("profile_iter", 1)
+    totals = dict(iter_ms=0.0, iter_seed_iters=0, iter_launches=0, launches=0, frames=0, seed_iters=0)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for k in range(args.steps):
+            fs, rs = step(k)
+            totals["iter_ms"] += rs["iter_ms"]
+            totals["iter_seed_iters"] += rs["iter_seed_iters"]
+            totals["iter_launches"] += rs["iter_launches"]
+            totals["launches"] += rs["launches"]
+            totals["frames"] += B
+            totals["seed_iters"] += sum(f["seed_iters"] for f in fs)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    ctx.set_option("profile_iter", 0)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.barrier()
+        ms = float(t.item())
+    frames_total = totals["frames"] * world
+    value = frames_total / (ms / 1e3)
+
+    # end-to-end through the host-pointer C-ABI entry (H2D + cluster + D2H inside the call)
+    e2e = None
+    if not args.no_e2e:
+        eh = torch.from_numpy(np.stack([f.emb for f in frames[:B]])).pin_memory()
+        lh = torch.empty((B, n), dtype=torch.int32).pin_memory()
+        ch = torch.empty((B, CAP, d), dtype=torch.float32).pin_memory()
+        ctx.cluster_host(eh, lh, ch, CAP, H, MAX_ITERS, None, pol, stream.cuda_stream)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        ksteps = max(1, min(args.steps, 10))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ksteps):
+            ctx.cluster_host(eh, lh, ch, CAP, H, MAX_ITERS, None, pol, stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": ksteps * B * world / (ems / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": B * n * d * 4, "d2h_bytes_per_step": B * n * 4 + B * CAP * d * 4}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    peaks, src = measured_peaks()
+    flops = totals["iter_seed_iters"] * n * 4 * d          # algorithmic: 4 n D per active seed-iteration
+    achieved = flops / (totals["iter_ms"] / 1e3) / 1e12 if totals["iter_ms"] > 0 else None
+    peak = peaks["bf16_tflops_sustained"]
+    roof = {"bound": "tensor", "kernel": "fms::iter_kernel<16> (K2)", "achieved": achieved, "peak": peak,
+            "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(),
+            "peak_source": f"{src} bf16 dense sustained (fp16 = bf16 rate); burst {peaks['bf16_tflops']}",
+            "flops_per_launch": flops / max(1, totals["iter_launches"]),
+            "ms_per_launch": totals["iter_ms"] / max(1, totals["iter_launches"]),
+            "iter_share_of_step": totals["iter_ms"] / ms if ms > 0 else None}
+    # frame-level roofline: algorithmic iteration FLOPs of the whole job at the tensor peak
+    frame_roof_ms = flops / (peak * 1e12) * 1e3
+    cb = None
+    if world == 1 and not args.no_cpu:
+        cb = cpu_baseline([synth.make_frame(args.config, 20000 + i) for i in range(3)], budget_s=20.0)
+    f0 = frames[0]
+    line = {
+        "metric": f"frames/sec ({f0.H}x{f0.W}, {d}-D embeddings) and mean-shift iteration % of roofline",
+        "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16x3 split / f32 accumulate", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {f0.H}x{f0.W} frame, {d}-D, {f0.cells} touching/overlapping cells "
+                               f"+ background, full OSOP (N_initial 128, gamma 0.9, L 2, P 0.99)",
+                   "frames_per_step": B, "l2": "2 alternating input batches of B x 16 MiB (> 126 MB L2)",
+                   "parallelism": f"replicas x{world}"},
+        "roofline": roof,
+        "frame_level_frac": frame_roof_ms / ms if ms > 0 else None,
+        "seed_iters_per_frame": totals["seed_iters"] / max(1, totals["frames"]),
+        "gpu_launches": totals["launches"],
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": cb,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

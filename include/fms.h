@@ -85,6 +85,7 @@ typedef struct {
   double iter_ms;             /* summed K2 device time over those launches (only if profiling on) */
   int64_t iter_seed_iters;    /* sum over K2 launches of active seeds (units of work) */
   int64_t iter_items;         /* sum over K2 launches of work items */
+  int64_t launches;           /* kernels this library launched during the call */
 } fms_run_stats;
 
 fms_status fms_default_policy(fms_seed_policy* out);

@@ -25,6 +25,8 @@ __device__ __forceinline__ float dotv(const float* a, const float* b) {
   return s;
 }
 
+constexpr int kKeptSm = 256;  // kept centres cached in SMEM during the greedy scan
+
 template <int DP>
 __global__ void __launch_bounds__(1024) merge_kernel(Params p) {
   const int f = blockIdx.x;
@@ -98,7 +100,10 @@ __global__ void __launch_bounds__(1024) merge_kernel(Params p) {
       __syncthreads();
     }
   }
-  // 3. greedy NMS in batches of 32
+  // 3. greedy NMS in batches of 32; batch candidates and the first kKeptSm kept centres live in
+  //    SMEM (after the sort buffers), so the serial in-batch chain never waits on global memory
+  float* cand = reinterpret_cast<float*>(vals + P2);            // [32][DP]
+  float* keptv = cand + 32 * DP;                                 // [kKeptSm][DP]
   const float thr = p.rho_f;  // keep unless x.c >= 1 - rho
   if (threadIdx.x == 0) { s_kept = 0; s_err = 0; }
   __syncthreads();
@@ -106,19 +111,24 @@ __global__ void __launch_bounds__(1024) merge_kernel(Params p) {
   for (int base = 0; base < P; base += 32) {
     const int nb = min(32, P - base);
     if (threadIdx.x == 0) s_supp = 0;
+    for (int t = threadIdx.x; t < nb * DP; t += blockDim.x) {
+      const int ci = t / DP, q = t - ci * DP;
+      cand[t] = pool[(size_t)vals[base + ci] * DP + q];
+    }
     __syncthreads();
     const int kept = s_kept;
     const int total = nb * kept;
     for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
       const int ci = idx / kept, k = idx - ci * kept;
-      if (dotv<DP>(pool + (size_t)vals[base + ci] * DP, cent + (size_t)k * DP) >= thr) atomicOr(&s_supp, 1u << ci);
+      const float* kv = k < kKeptSm ? keptv + k * DP : cent + (size_t)k * DP;
+      if (dotv<DP>(cand + ci * DP, kv) >= thr) atomicOr(&s_supp, 1u << ci);
     }
     __syncthreads();
     if (warp == 0) {
-      const float* a = lane < nb ? pool + (size_t)vals[base + lane] * DP : pool;
+      const float* a = cand + (lane < nb ? lane : 0) * DP;
       unsigned inb = 0;
       for (int j = 0; j < nb; ++j)
-        if (j < lane && dotv<DP>(a, pool + (size_t)vals[base + j] * DP) >= thr) inb |= 1u << j;
+        if (j < lane && dotv<DP>(a, cand + j * DP) >= thr) inb |= 1u << j;
       const unsigned supp = s_supp;
       unsigned keep = 0;
       for (int i = 0; i < nb; ++i) {
@@ -128,7 +138,10 @@ __global__ void __launch_bounds__(1024) merge_kernel(Params p) {
       if (lane < nb && ((keep >> lane) & 1u)) {
         const int pos = kept + __popc(keep & ((1u << lane) - 1u));
         if (pos < p.C_cap) {
-          for (int q = 0; q < DP; ++q) cent[(size_t)pos * DP + q] = a[q];
+          for (int q = 0; q < DP; ++q) {
+            cent[(size_t)pos * DP + q] = a[q];
+            if (pos < kKeptSm) keptv[pos * DP + q] = a[q];
+          }
           p.cint[(size_t)f * p.C_cap + pos] = pint[vals[base + lane]];
           p.corig[(size_t)f * p.C_cap + pos] = porg[vals[base + lane]];
         } else {
@@ -278,21 +291,22 @@ __global__ void output_kernel(Params p, float* centres_out, int cap) {
   }
 }
 
-int merge_smem_bytes(int P_cap) {
+int merge_smem_bytes(int P_cap, int DP) {
   int P2 = 1;
   while (P2 < P_cap) P2 <<= 1;
-  return P2 * 12;
+  return P2 * 12 + (32 + kKeptSm) * DP * 4;
 }
 
 cudaError_t setup_post_attrs(int P_cap) {
-  const int sm = merge_smem_bytes(P_cap);
-  cudaError_t e = cudaFuncSetAttribute(merge_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaError_t e = cudaFuncSetAttribute(merge_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       merge_smem_bytes(P_cap, 16));
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(merge_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  return cudaFuncSetAttribute(merge_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              merge_smem_bytes(P_cap, 32));
 }
 
 cudaError_t launch_post(const Params& p, cudaStream_t st) {
-  const int sm = merge_smem_bytes(p.P_cap);
+  const int sm = merge_smem_bytes(p.P_cap, p.DP);
   dim3 ga((unsigned)((p.n + 255) / 256), p.B);
   if (p.DP == 16) {
     merge_kernel<16><<<p.B, 1024, sm, st>>>(p);

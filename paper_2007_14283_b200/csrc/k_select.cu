@@ -1,8 +1,9 @@
 // k_select.cu -- K1 (normalise + quantise) and K6 (OSOP seed selection).
 //
 // K1: Eq. 1 / Eq. 9 -- every embedding is divided by its norm; the
-//     unit vector is stored in fp16 as the tensor-core operand (row padded to DP, frame padded to a
-//     whole number of 128-pixel tiles with zero rows, which never enter a window since tau > 0).
+//     unit vector is stored as two fixed-point limbs (integers held exactly in fp16, x ~= (hi +
+//     lo 2^-11) 2^-11, |err| <= 2^-23) as the tensor-core operand (rows padded to DP, frames padded
+//     to whole 128-pixel tiles with zero rows, which never enter a window since tau > 0).
 // K6: Alg. 2 line 2 ("Evenly random select seed vector set"), reading R11: the K_r candidate
 //     pixels with the smallest splitmix64 keys, in ascending pixel order.  Candidates are all pixels
 //     in round 0 and the uncovered, unvisited pixels afterwards (north_star / R13).
@@ -33,6 +34,7 @@ __global__ void prep_kernel(Params p) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.n_pad) return;
   __align__(16) __half h[DP];
+  __align__(16) __half l[DP];
   if (i < p.n) {
     const float* x = p.emb + ((size_t)f * p.n + i) * p.d;
     float v[DP];
@@ -50,17 +52,20 @@ __global__ void prep_kernel(Params p) {
       inv = 1.0f / nrm;
     }
 #pragma unroll
-    for (int k = 0; k < DP; ++k) h[k] = __float2half_rn(v[k] * inv);
+    for (int k = 0; k < DP; ++k) limbs(v[k] * inv, h[k], l[k]);
     p.inv[(size_t)f * p.n + i] = inv;
     p.flags[(size_t)f * p.n + i] = 0;
   } else {
 #pragma unroll
-    for (int k = 0; k < DP; ++k) h[k] = __float2half_rn(0.f);
+    for (int k = 0; k < DP; ++k) h[k] = l[k] = __float2half_rn(0.f);
   }
   uint4* dst = reinterpret_cast<uint4*>(p.Xh + ((size_t)f * p.n_pad + i) * DP);
-  const uint4* src = reinterpret_cast<const uint4*>(h);
+  uint4* dstl = reinterpret_cast<uint4*>(p.Xl + ((size_t)f * p.n_pad + i) * DP);
 #pragma unroll
-  for (int k = 0; k < DP / 8; ++k) dst[k] = src[k];
+  for (int k = 0; k < DP / 8; ++k) {
+    dst[k] = reinterpret_cast<const uint4*>(h)[k];
+    dstl[k] = reinterpret_cast<const uint4*>(l)[k];
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -252,12 +257,18 @@ __global__ void sel_write_kernel(Params p) {
     const float* x = p.emb + ((size_t)f * p.n + i) * p.d;
     float* s = p.seeds + so * DP;
     __half* sh = p.sop + ((size_t)f * p.S_pad + pos) * DP;
+    __half* ss = p.sops + ((size_t)f * p.S_pad + pos) * DP;
+    __half* sl = p.sopl + ((size_t)f * p.S_pad + pos) * DP;
 #pragma unroll
     for (int k = 0; k < DP; ++k) {
       float v = k < p.d ? x[k] * inv : 0.f;
       s[k] = v;
-      sh[k] = __float2half_rn(v);
+      split_seed(v, sh[k], ss[k], sl[k]);
     }
+    double* g = p.gacc + ((size_t)f * p.S_pad + pos) * DP;
+#pragma unroll
+    for (int k = 0; k < DP; ++k) g[k] = 0.0;
+    p.cacc[(size_t)f * p.S_pad + pos] = 0;
     p.sorig[so] = (int)i;
     p.sstat[so] = ST_ACTIVE;
     p.scnt[so] = 0;
@@ -283,14 +294,14 @@ __global__ void sel_finish_kernel(Params p) {
   c.total += K;
   c.round_K[c.round] = K;
   c.round_seed_iters[c.round] = 0;
-  // split-pixel factor: fixed for the round, from the frame's own K_r (independent of batching)
-  const int tiles = (K + kBM - 1) / kBM;
-  int splits = kItemTarget / (tiles > 0 ? tiles : 1);
-  if (splits < 1) splits = 1;
-  if (splits > p.n_ptiles) splits = p.n_ptiles;
-  c.chunk_tiles = (p.n_ptiles + splits - 1) / splits;
-  c.splits = (p.n_ptiles + c.chunk_tiles - 1) / c.chunk_tiles;
   if (K == 0) { c.phase = PH_POST; }
+  // rows [K, roundup(K, 128)) of the last seed tile are computed too; start them at zero
+  const int kpad = (K + kBM - 1) / kBM * kBM;
+  for (int r = K; r < kpad && r < p.S_pad; ++r) {
+    double* g = p.gacc + ((size_t)f * p.S_pad + r) * p.DP;
+    for (int k = 0; k < p.DP; ++k) g[k] = 0.0;
+    p.cacc[(size_t)f * p.S_pad + r] = 0;
+  }
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -2,52 +2,45 @@
 // converge), and the per-frame early-stop / compaction step.
 //
 // K3 implements, for every active seed (R4, R6):
-//     G = sum over split-pixel partials in fixed split order (fp64)
+//     G = the exact windowed sum merged by K2 (fp64 accumulator, reset after reading)
 //     s' = G / |G|                      (renormalised onto the unit sphere; the count cancels)
 //     delta = |s' - s|_2,  converged if delta < tol = h/1000,  converged seeds freeze (R9)
 //     window count 0 -> stalled (never happens for seeds started at pixels, pin P3)
 // ctl_step applies early stopping (R8): once converged >= ceil(gamma*K_r) or no seed is
-// active (or max_iter), the remaining active seeds are discarded and the frame moves to the merge
-// phase; otherwise the active seeds are compacted (ascending seed index) into the fp16 operand rows.
+// active (or max_iter), the remaining active seeds are discarded and the converged modes get one
+// count pass (their intensity |S_h(m)|, R10) before the merge phase; otherwise the active seeds
+// are compacted (ascending seed index) into the fp16 hi/lo operand rows.
 #include "fms_device.cuh"
 
 namespace fms {
 
-// one CTA: prefix over frames -> item table and tile-task table for this step
+// one CTA: prefix over frames -> tile-task table for this step.  Work item i is chunk
+// (i mod n_chunks) of tile task (i div n_chunks).
 __global__ void plan_kernel(Params p) {
   __shared__ int sm[33];
-  __shared__ int s_items_total, s_tiles_total;
-  int carry_i = 0, carry_t = 0;
+  __shared__ int s_tiles_total;
+  int carry_t = 0;
   for (int f0 = 0; f0 < p.B; f0 += blockDim.x) {
     const int f = f0 + threadIdx.x;
-    int ni = 0, nt = 0;
+    int nt = 0;
     if (f < p.B) {
       FrameCtl& c = p.ctl[f];
-      if (c.phase == PH_ITERATE && c.n_active > 0) {
-        nt = (c.n_active + kBM - 1) / kBM;
-        ni = nt * c.splits;
-      }
+      if ((c.phase == PH_ITERATE || c.phase == PH_COUNT) && c.n_active > 0) nt = (c.n_active + kBM - 1) / kBM;
     }
-    int ti, tt;
-    int oi = block_excl_scan(ni, sm, &ti);
-    int ot = block_excl_scan(nt, sm, &tt);
+    int tt;
+    const int ot = block_excl_scan(nt, sm, &tt);
     if (f < p.B) {
       FrameCtl& c = p.ctl[f];
-      c.item_off = carry_i + oi;
       c.tile_off = carry_t + ot;
       c.n_tiles_step = nt;
       c.step_conv = 0;
       c.step_stall = 0;
     }
-    carry_i += ti;
     carry_t += tt;
   }
-  if (threadIdx.x == 0) {
-    s_items_total = carry_i;
-    s_tiles_total = carry_t;
-  }
+  if (threadIdx.x == 0) s_tiles_total = carry_t;
   __syncthreads();
-  if (s_items_total > p.items_cap || s_tiles_total > p.tiles_cap) {
+  if (s_tiles_total > p.tiles_cap) {
     if (threadIdx.x == 0) { p.counters[0] = 0; p.counters[1] = 0; p.counters[5] = 1; }
     return;
   }
@@ -55,24 +48,16 @@ __global__ void plan_kernel(Params p) {
   for (int f = warp; f < p.B; f += nw) {
     const FrameCtl& c = p.ctl[f];
     const int nt = c.n_tiles_step;
-    if (nt == 0) continue;
-    const int S = c.splits, ch = c.chunk_tiles;
-    for (int idx = lane; idx < nt * S; idx += 32) {
-      const int tile = idx / S, s = idx % S;
-      const int begin = s * ch;
-      int cnt = p.n_ptiles - begin;
-      if (cnt > ch) cnt = ch;
-      p.items[c.item_off + idx] = WorkItem{f, tile, begin, cnt};
-    }
-    for (int tile = lane; tile < nt; tile += 32) p.tiles[c.tile_off + tile] = TileTask{f, tile, c.item_off + tile * S, S};
+    const int mode = c.phase == PH_COUNT ? 1 : 0;
+    for (int tile = lane; tile < nt; tile += 32) p.tiles[c.tile_off + tile] = TileTask{f, tile, 0, 0, mode, 0, 0, 0};
   }
   if (threadIdx.x == 0) {
-    p.counters[0] = s_items_total;
+    p.counters[0] = s_tiles_total * p.n_chunks;
     p.counters[1] = s_tiles_total;
     p.counters[3] = 0;
     long long units = 0;
     for (int f = 0; f < p.B; ++f)
-      if (p.ctl[f].n_tiles_step) units += p.ctl[f].n_active;
+      if (p.ctl[f].n_tiles_step && p.ctl[f].phase == PH_ITERATE) units += p.ctl[f].n_active;
     reinterpret_cast<long long*>(p.counters + 6)[0] = units;  // active seeds this step (A_t summed)
   }
 }
@@ -85,43 +70,41 @@ __global__ void __launch_bounds__(kBM) update_kernel(Params p) {
     FrameCtl& c = p.ctl[task.f];
     const int j = task.tile * kBM + threadIdx.x;
     int conv = 0, stall = 0;
-    if (j < c.n_active) {
-      const size_t sidx = (size_t)task.f * p.S_cap + p.act[(size_t)task.f * p.S_cap + j];
+    const size_t r = (size_t)task.f * p.S_pad + j;  // compacted row (accumulator index)
+    if (task.mode == 1) {
+      // count pass: intensity |S_h(m)| of a converged mode (R10)
+      if (j < c.n_active) p.scnt[(size_t)task.f * p.S_cap + p.act[(size_t)task.f * p.S_cap + j]] = p.cacc[r];
+      p.cacc[r] = 0;
+    } else {
       double g[DP];
 #pragma unroll
-      for (int k = 0; k < DP; ++k) g[k] = 0.0;
-      long long cnt = 0;
-      for (int s = 0; s < task.splits; ++s) {
-        const size_t row = (size_t)(task.item0 + s) * kBM + threadIdx.x;
-        const float4* src = reinterpret_cast<const float4*>(p.part_g + row * DP);
-#pragma unroll
-        for (int q = 0; q < DP / 4; ++q) {
-          const float4 v = src[q];
-          g[4 * q] += v.x; g[4 * q + 1] += v.y; g[4 * q + 2] += v.z; g[4 * q + 3] += v.w;
-        }
-        cnt += p.part_c[row];
+      for (int k = 0; k < DP; ++k) {
+        g[k] = p.gacc[r * DP + k];
+        p.gacc[r * DP + k] = 0.0;  // every row of a processed tile is reset for the next step
       }
-      if (cnt == 0) {
-        p.sstat[sidx] = ST_STALLED;
-        stall = 1;
-      } else {
+      if (j < c.n_active) {
+        const size_t sidx = (size_t)task.f * p.S_cap + p.act[(size_t)task.f * p.S_cap + j];
         double nn = 0.0;
 #pragma unroll
         for (int k = 0; k < DP; ++k) nn += g[k] * g[k];
-        const double rn = 1.0 / sqrt(nn);
-        float* s = p.seeds + sidx * DP;
-        double dd = 0.0;
+        if (!(nn > 0.0)) {
+          p.sstat[sidx] = ST_STALLED;  // empty window: the 0/1-weighted sum is exactly zero
+          stall = 1;
+        } else {
+          const double rn = 1.0 / sqrt(nn);
+          float* s = p.seeds + sidx * DP;
+          double dd = 0.0;
 #pragma unroll
-        for (int k = 0; k < DP; ++k) {
-          const double v = g[k] * rn;
-          const double e = v - (double)s[k];
-          dd += e * e;
-          s[k] = (float)v;
-        }
-        p.scnt[sidx] = (int)cnt;
-        if (sqrt(dd) < p.tol) {
-          p.sstat[sidx] = ST_CONV;
-          conv = 1;
+          for (int k = 0; k < DP; ++k) {
+            const double v = g[k] * rn;
+            const double e = v - (double)s[k];
+            dd += e * e;
+            s[k] = (float)v;
+          }
+          if (sqrt(dd) < p.tol) {
+            p.sstat[sidx] = ST_CONV;
+            conv = 1;
+          }
         }
       }
     }
@@ -135,13 +118,51 @@ __global__ void __launch_bounds__(kBM) update_kernel(Params p) {
   }
 }
 
+// compact the seeds of frame f with status `want` (ascending seed index) into act / fp16 rows
+template <int DP>
+__device__ int compact_seeds(const Params& p, int f, int K, uint8_t want, int* sm) {
+  const size_t base = (size_t)f * p.S_cap;
+  int carry = 0;
+  for (int j0 = 0; j0 < K; j0 += blockDim.x) {
+    const int j = j0 + threadIdx.x;
+    const int a = (j < K && p.sstat[base + j] == want) ? 1 : 0;
+    int tot;
+    const int pos = carry + block_excl_scan(a, sm, &tot);
+    if (a) {
+      p.act[base + pos] = j;
+      const float* s = p.seeds + (base + j) * DP;
+      __align__(16) __half h[DP];
+      __align__(16) __half hs[DP];
+      __align__(16) __half l[DP];
+#pragma unroll
+      for (int k = 0; k < DP; ++k) split_seed(s[k], h[k], hs[k], l[k]);
+      const size_t ro = (size_t)f * p.S_pad + pos;
+      uint4* dst = reinterpret_cast<uint4*>(p.sop + ro * DP);
+      uint4* dsts = reinterpret_cast<uint4*>(p.sops + ro * DP);
+      uint4* dstl = reinterpret_cast<uint4*>(p.sopl + ro * DP);
+#pragma unroll
+      for (int k = 0; k < DP / 8; ++k) {
+        dst[k] = reinterpret_cast<const uint4*>(h)[k];
+        dsts[k] = reinterpret_cast<const uint4*>(hs)[k];
+        dstl[k] = reinterpret_cast<const uint4*>(l)[k];
+      }
+    }
+    carry += tot;
+  }
+  return carry;
+}
+
 template <int DP>
 __global__ void ctl_step_kernel(Params p) {
   const int f = blockIdx.x;
   FrameCtl& c = p.ctl[f];
-  if (c.phase != PH_ITERATE) return;
   __shared__ int s_end, s_rem;
   __shared__ int sm[33];
+  if (c.phase == PH_COUNT) {  // intensities written by the update kernel
+    if (threadIdx.x == 0) { c.phase = PH_POST; c.n_active = 0; }
+    return;
+  }
+  if (c.phase != PH_ITERATE) return;
   if (threadIdx.x == 0) {
     const int A = c.n_active;
     c.t += 1;
@@ -158,40 +179,28 @@ __global__ void ctl_step_kernel(Params p) {
   if (s_end) {
     for (int j = threadIdx.x; j < K; j += blockDim.x)
       if (p.sstat[base + j] == ST_ACTIVE) p.sstat[base + j] = ST_DISCARDED;
+    __syncthreads();
+    const int r = c.round;
+    const int nconv = c.n_conv;
+    if (nconv > 0) compact_seeds<DP>(p, f, K, ST_CONV, sm);  // rows for the intensity pass
     if (threadIdx.x == 0) {
-      const int r = c.round;
       c.round_iters[r] = c.t;
-      c.round_conv[r] = c.n_conv;
-      c.round_disc[r] = K - c.n_conv;
-      c.n_active = 0;
-      if (r == 0 && c.n_conv == 0) {
+      c.round_conv[r] = nconv;
+      c.round_disc[r] = K - nconv;
+      c.n_active = nconv;
+      if (r == 0 && nconv == 0) {
         c.status = 4;  // FMS_E_STALLED
         c.phase = PH_ERROR;
+      } else if (nconv > 0) {
+        c.phase = PH_COUNT;
+        atomicAdd(&p.counters[3], 1);
       } else {
         c.phase = PH_POST;
       }
     }
     return;
   }
-  // compact the active seeds (ascending seed index) and rebuild their fp16 operand rows
-  int carry = 0;
-  for (int j0 = 0; j0 < K; j0 += blockDim.x) {
-    const int j = j0 + threadIdx.x;
-    const int a = (j < K && p.sstat[base + j] == ST_ACTIVE) ? 1 : 0;
-    int tot;
-    const int pos = carry + block_excl_scan(a, sm, &tot);
-    if (a) {
-      p.act[base + pos] = j;
-      const float* s = p.seeds + (base + j) * DP;
-      __align__(16) __half h[DP];
-#pragma unroll
-      for (int k = 0; k < DP; ++k) h[k] = __float2half_rn(s[k]);
-      uint4* dst = reinterpret_cast<uint4*>(p.sop + ((size_t)f * p.S_pad + pos) * DP);
-#pragma unroll
-      for (int k = 0; k < DP / 8; ++k) dst[k] = reinterpret_cast<const uint4*>(h)[k];
-    }
-    carry += tot;
-  }
+  const int carry = compact_seeds<DP>(p, f, K, ST_ACTIVE, sm);
   if (threadIdx.x == 0) {
     c.n_active = carry;
     atomicAdd(&p.counters[3], 1);  // frames still iterating

@@ -27,8 +27,7 @@ namespace fms {
 cudaError_t launch_prep(const Params& p, cudaStream_t st);
 cudaError_t launch_select(const Params& p, int num_sms, cudaStream_t st);
 cudaError_t launch_plan(const Params& p, cudaStream_t st);
-cudaError_t launch_iter(int DP, const CUtensorMap& tx, const CUtensorMap& ts, const Params& p, int grid,
-                        cudaStream_t st);
+cudaError_t launch_iter(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st);
 cudaError_t launch_update_ctl(const Params& p, int num_sms, cudaStream_t st);
 cudaError_t launch_post(const Params& p, cudaStream_t st);
 cudaError_t launch_output(const Params& p, float* centres_out, int cap, cudaStream_t st);
@@ -41,7 +40,7 @@ using namespace fms;
 namespace {
 
 constexpr int kPoll = 4;            // lockstep steps launched between host polls
-constexpr int kMaxPcap = 16384;     // merge pool capacity (SMEM bitonic sort)
+constexpr int kMaxPcap = 8192;      // merge pool capacity (SMEM bitonic sort)
 constexpr int kCounters = 64;
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -52,6 +51,8 @@ struct Ctx {
   std::string err;
   bool profile = false;
   bool attrs_done = false;
+  bool fresh_ws = true;
+  size_t last_layout = 0;
   // device workspace (one allocation, carved per call)
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -131,10 +132,15 @@ size_t carve(Params& p, uint8_t* base) {
   };
   const size_t B = p.B;
   p.Xh = (__half*)take(B * p.n_pad * p.DP * 2);
+  p.Xl = (__half*)take(B * p.n_pad * p.DP * 2);
   p.inv = (float*)take(B * p.n * 4);
   p.flags = (uint8_t*)take(B * p.n);
   p.seeds = (float*)take(B * (size_t)p.S_cap * p.DP * 4);
   p.sop = (__half*)take(B * (size_t)p.S_pad * p.DP * 2);
+  p.sops = (__half*)take(B * (size_t)p.S_pad * p.DP * 2);
+  p.sopl = (__half*)take(B * (size_t)p.S_pad * p.DP * 2);
+  p.gacc = (double*)take(B * (size_t)p.S_pad * p.DP * 8);
+  p.cacc = (int*)take(B * (size_t)p.S_pad * 4);
   p.sorig = (int*)take(B * (size_t)p.S_cap * 4);
   p.sstat = (uint8_t*)take(B * (size_t)p.S_cap);
   p.scnt = (int*)take(B * (size_t)p.S_cap * 4);
@@ -146,9 +152,6 @@ size_t carve(Params& p, uint8_t* base) {
   p.pool = (float*)take(B * (size_t)p.P_cap * p.DP * 4);
   p.pint = (int*)take(B * (size_t)p.P_cap * 4);
   p.porg = (int*)take(B * (size_t)p.P_cap * 4);
-  p.part_g = (float*)take((size_t)p.items_cap * kBM * p.DP * 4);
-  p.part_c = (int*)take((size_t)p.items_cap * kBM * 4);
-  p.items = (WorkItem*)take((size_t)p.items_cap * sizeof(WorkItem));
   p.tiles = (TileTask*)take((size_t)p.tiles_cap * sizeof(TileTask));
   p.counters = (int*)take(kCounters * 4);
   p.sample = (unsigned long long*)take(B * (size_t)p.sample_cap * 8);
@@ -185,7 +188,8 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   p.C_cap = (int)std::min<long long>(n, 65536);
   p.P_cap = (int)std::min<long long>((long long)p.C_cap + p.S_cap, kMaxPcap);
   p.tiles_cap = B * (p.S_pad / kBM);
-  p.items_cap = B * std::max(kItemTarget, p.S_pad / kBM);
+  p.n_chunks = (p.n_ptiles + kChunkTiles - 1) / kChunkTiles;
+  p.items_cap = p.tiles_cap * p.n_chunks;
   p.sample_cap = (int)std::min<long long>(n, (long long)S + 8 * (long long)std::sqrt((double)S) + 1024);
   p.nblk = (int)((n + 2047) / 2048);
   p.h = h;
@@ -217,6 +221,11 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
       return fail(c, FMS_E_OOM, "workspace allocation of " + std::to_string(need) + " bytes failed");
     }
     c->ws_bytes = need;
+    c->fresh_ws = true;
+  }
+  if (c->last_layout != need + (size_t)B * 1000003u + (size_t)p.S_pad * 7u) {
+    c->fresh_ws = true;  // a different carve moves the accumulators
+    c->last_layout = need + (size_t)B * 1000003u + (size_t)p.S_pad * 7u;
   }
   carve(p, reinterpret_cast<uint8_t*>(c->ws));
   if ((size_t)B > c->h_ctl_cap) {
@@ -226,19 +235,28 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   }
   if (!c->h_counters) CU(cudaMallocHost(&c->h_counters, kCounters * 4));
 
-  CUtensorMap tmx, tms;
-  fms_status ts = make_tmap(c, &tmx, p.Xh, (uint64_t)B * p.n_pad, p.DP);
-  if (ts != FMS_OK) return ts;
-  ts = make_tmap(c, &tms, p.sop, (uint64_t)B * p.S_pad, p.DP);
+  TMaps tm;
+  fms_status ts = make_tmap(c, &tm.xh, p.Xh, (uint64_t)B * p.n_pad, p.DP);
+  if (ts == FMS_OK) ts = make_tmap(c, &tm.xl, p.Xl, (uint64_t)B * p.n_pad, p.DP);
+  if (ts == FMS_OK) ts = make_tmap(c, &tm.sh, p.sop, (uint64_t)B * p.S_pad, p.DP);
+  if (ts == FMS_OK) ts = make_tmap(c, &tm.ss, p.sops, (uint64_t)B * p.S_pad, p.DP);
+  if (ts == FMS_OK) ts = make_tmap(c, &tm.sl, p.sopl, (uint64_t)B * p.S_pad, p.DP);
   if (ts != FMS_OK) return ts;
 
   CU(cudaEventRecord(c->t0, st));
   CU(cudaMemsetAsync(p.counters, 0, kCounters * 4, st));
+  if (c->fresh_ws) {  // accumulator rows are kept zero between steps by K3; start clean once
+    CU(cudaMemsetAsync(p.gacc, 0, (size_t)B * p.S_pad * p.DP * 8, st));
+    CU(cudaMemsetAsync(p.cacc, 0, (size_t)B * p.S_pad * 4, st));
+    c->fresh_ws = false;
+  }
   CU(launch_prep(p, st));
   int steps = 0, launches = 0;
+  long long kernels = 2;  // init + prep
   std::vector<int> prof_slots;
   for (int round = 0; round < pol->max_rounds + 1; ++round) {
     CU(launch_select(p, c->num_sms, st));
+    kernels += 7;
     for (int s = 0; s < max_iters + kPoll; s += kPoll) {
       for (int k = 0; k < kPoll; ++k) {
         CU(launch_plan(p, st));
@@ -264,15 +282,16 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
             c->h_prof_cap = ncap;
           }
           CU(cudaEventRecord(c->ev[2 * slot], st));
-          CU(launch_iter(p.DP, tmx, tms, p, c->num_sms, st));
+          CU(launch_iter(p.DP, tm, p, c->num_sms, st));
           CU(cudaEventRecord(c->ev[2 * slot + 1], st));
           CU(cudaMemcpyAsync(c->h_prof + slot * 8, p.counters, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
           ++launches;
         } else {
-          CU(launch_iter(p.DP, tmx, tms, p, c->num_sms, st));
+          CU(launch_iter(p.DP, tm, p, c->num_sms, st));
         }
         CU(launch_update_ctl(p, c->num_sms, st));
         ++steps;
+        kernels += 4;  // plan, iter, update, ctl_step
       }
       CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
       CU(cudaStreamSynchronize(st));
@@ -280,11 +299,15 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
       if (c->h_counters[3] == 0) break;  // no frame still iterating
     }
     CU(launch_post(p, st));
+    kernels += 3;
     CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (c->h_counters[2] == 0) break;  // every frame DONE (or in error)
   }
-  if (cap > 0) CU(launch_output(p, centres, cap, st));
+  if (cap > 0) {
+    CU(launch_output(p, centres, cap, st));
+    kernels += 1;
+  }
   CU(cudaEventRecord(c->t1, st));
   CU(cudaMemcpyAsync(c->h_ctl, p.ctl, sizeof(FrameCtl) * B, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
@@ -334,6 +357,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
     rs->ms_total = ms;
     rs->workspace_bytes = (int64_t)c->ws_bytes;
     rs->steps = steps;
+    rs->launches = kernels;
     if (c->profile) {
       for (int l = 0; l < launches; ++l) {
         const int* snap = c->h_prof + (size_t)l * 8;
