@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -210,6 +211,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   p.rng_seed = pol->rng_seed;
   p.emb = emb;
   p.labels = labels;
+  if (const char* v = getenv("FMS_ITER_VARIANT")) p.variant = atoi(v);  // timing experiments only
 
   const size_t need = carve(p, nullptr);
   if (need > c->ws_bytes) {
