@@ -1,0 +1,83 @@
+"""Summarise ncu captures into profiles/ (runs on the CPU box).
+
+  python tools/ncu_summary.py launches gpurun_out/launches.csv profiles/launches_r01.md
+  python tools/ncu_summary.py full gpurun_out/prof_iter.ncu-rep profiles/iter_kernel_ncu.json [launch-index]
+"""
+import collections
+import csv
+import io
+import json
+import subprocess
+import sys
+
+UNIT = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
+
+
+def launches(src, dst):
+    rows = list(csv.reader(open(src)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[hi]
+    ki, mi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    tot, cnt = collections.defaultdict(float), collections.Counter()
+    for r in rows[hi + 1:]:
+        if len(r) <= mi or not r[mi]:
+            continue
+        us = float(r[mi].replace(",", "")) * UNIT.get(r[ui], 1.0)
+        name = r[ki].split("(")[0].replace("void ", "").strip()
+        tot[name] += us
+        cnt[name] += 1
+    T = sum(tot.values())
+    out = ["| kernel | launches | total us | share | avg us |", "|---|---|---|---|---|"]
+    for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+        out.append(f"| `{k}` | {cnt[k]} | {v:.1f} | {100 * v / T:.1f}% | {v / cnt[k]:.2f} |")
+    out.append(f"\nTotal device time over {sum(cnt.values())} launches: {T:.1f} us "
+               "(ncu serialised, cold-cache per launch: compare shares, not absolutes).")
+    open(dst, "w").write("\n".join(out) + "\n")
+    print("\n".join(out))
+
+
+def full(src, dst, idx=0):
+    raw = subprocess.check_output(["ncu", "-i", src, "--page", "raw", "--csv"], text=True)
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    d = dict(zip(hdr, rows[2 + idx]))
+    u = dict(zip(hdr, units))
+
+    def f(k, scale=1.0):
+        v = d.get(k, "")
+        try:
+            return float(v.replace(",", "")) * scale
+        except ValueError:
+            return None
+
+    def bytes_(k):
+        v = f(k)
+        if v is None:
+            return None
+        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u.get(k, "byte"), 1)
+        return v * mult
+
+    dur_us = f("gpu__time_duration.sum") * (1e-3 if u.get("gpu__time_duration.sum") == "nsecond" else 1.0)
+    rd, wr = bytes_("dram__bytes_read.sum"), bytes_("dram__bytes_write.sum")
+    summary = {
+        "kernel": d.get("Kernel Name", ""),
+        "duration_us": dur_us,
+        "dram_bytes_read": rd, "dram_bytes_write": wr,
+        "dram_bytes_per_launch": (rd or 0) + (wr or 0),
+        "sm_cycles_active_avg": f("sm__cycles_active.avg"),
+        "sm_cycles_elapsed_avg": f("sm__cycles_elapsed.avg"),
+        "tensor_pipe_active_pct_of_peak_elapsed":
+            f("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
+        "registers_per_thread": f("launch__registers_per_thread"),
+        "threads_per_block": f("launch__block_size"),
+        "source": src,
+    }
+    json.dump(summary, open(dst, "w"), indent=1)
+    print(json.dumps(summary, indent=1))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2], sys.argv[3])
+    else:
+        full(sys.argv[2], sys.argv[3], int(sys.argv[4]) if len(sys.argv) > 4 else 0)
