@@ -107,6 +107,18 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+def reduce_max(x: float, world: int, device=None) -> float:
+    """Max over ranks of a per-rank time (barrier first); identity on one rank."""
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.barrier()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -143,7 +155,7 @@ def cpu_baseline(frames, budget_s=20.0):
 
 
 def run_reference(args, world, rank):
-    if rank != 0:
+    if rank != 0:  # the reference arm runs on rank 0 only; other ranks exit 0 without work
         return
     import synth
     frames = [synth.make_frame(args.config, 1000 + i) for i in range(max(1, args.steps + args.warmup))]
@@ -214,13 +226,8 @@ def main():
             totals["seed_iters"] += sum(f["seed_iters"] for f in fs)
         ev1.record(stream)
         torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    ms = reduce_max(ev0.elapsed_time(ev1), world, dev)
     ctx.set_option("profile_iter", 0)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.barrier()
-        ms = float(t.item())
     frames_total = totals["frames"] * world
     value = frames_total / (ms / 1e3)
 
@@ -241,11 +248,7 @@ def main():
             ctx.cluster_host(eh, lh, ch, CAP, H, MAX_ITERS, None, pol, stream.cuda_stream)
         e1.record(stream)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ems], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = reduce_max(e0.elapsed_time(e1), world, dev)
         e2e = {"value": ksteps * B * world / (ems / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": B * n * d * 4, "d2h_bytes_per_step": B * n * 4 + B * CAP * d * 4}
 
