@@ -70,6 +70,8 @@ int main(int argc, char** argv) {
   cudaMemcpy(p.counters, cnt, 8, cudaMemcpyHostToDevice);
   cudaMalloc(&p.gacc, B * S_pad * DP * 8);
   cudaMalloc(&p.cacc, B * S_pad * 4);
+  cudaMalloc(&p.dbg, 16 * 512 * 8 * 8);
+  cudaMemset(p.dbg, 0, 16 * 512 * 8 * 8);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   const double pairs = (double)T * 128 * n;
@@ -86,10 +88,31 @@ int main(int argc, char** argv) {
     cudaEventElapsedTime(&ms, e0, e1);
     ms /= reps;
     const double tiles_per_sm = (double)T * p.n_ptiles / 148.0;
-    printf("B=%d T/frame=%d variant %2d (%s%s%s%s%s): %.3f ms/launch, %.0f ns per 128x128 tile per SM, %.1f TFLOP/s (4nD/pair)\n", B, T_per_frame, v,
+    printf("B=%d T/frame=%d variant %2d (%s%s%s%s%s%s): %.3f ms/launch, %.0f ns per 128x128 tile per SM, %.1f TFLOP/s (4nD/pair)\n", B, T_per_frame, v,
            (v & 1) ? "noMMA2 " : "", (v & 2) ? "noEpi " : "", (v & 4) ? "1termMMA1 " : "", (v & 8) ? "noMMA1 " : "",
            (v & 16) ? "noLDTM " : "", (v & 64) ? "noTMA" : "", ms,
            ms * 1e6 / tiles_per_sm, pairs * 64 / (ms * 1e-3) / 1e12);
+  }
+  // event timeline of CTA 0 for the full kernel
+  p.variant = argc > 4 ? atoi(argv[4]) : 256;
+  launch_iter(DP, tm, p, 148, 0);
+  cudaDeviceSynchronize();
+  std::vector<long long> h(16 * 512 * 8);
+  cudaMemcpy(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost);
+  auto ev = [&](int role, int t, int e) { return h[((size_t)role * 512 + t) * 8 + e]; };
+  const long long t0 = ev(1, 0, 0);
+  printf("tile | prod xempty | MMA1 start cempty xfull commit | per-warp epilogue: cfull, then deltas: cfull-wait, load+release, compute, P-free wait, STTM, issue\n");
+  for (int t = 0; t < 40; ++t) {
+    printf("%3d | %6lld | %6lld %6lld %6lld %6lld |", t, ev(0, t, 0) - t0, ev(1, t, 0) - t0, ev(1, t, 1) - t0,
+           ev(1, t, 2) - t0, ev(1, t, 3) - t0);
+    const int g = t & 1;
+    for (int q = 0; q < 4; ++q) {
+      const int role = 3 + g * 4 + q;
+      printf(" q%d %6lld %4lld %4lld %4lld %4lld %4lld %4lld |", q, ev(role, t, 1) - t0, ev(role, t, 1) - ev(role, t, 0), ev(role, t, 2) - ev(role, t, 1),
+             ev(role, t, 5) - ev(role, t, 2), ev(role, t, 6) - ev(role, t, 5), ev(role, t, 3) - ev(role, t, 6),
+             ev(role, t, 4) - ev(role, t, 3));
+    }
+    printf("\n");
   }
   return 0;
 }
