@@ -39,10 +39,14 @@
 
 namespace fms {
 
-constexpr int kEpiWarps = 8;                            // 2 groups x 4 warps (one per TMEM lane quarter)
-constexpr int kGroupWarps = 4;                           // a group owns every other pixel tile
-constexpr int kEpiWarp0 = 3;                             // warps: 0 TMA, 1 MMA1, 2 MMA2, 3..10 epilogue
-constexpr int kIterThreads = (kEpiWarp0 + kEpiWarps) * 32;
+// Epilogue: two groups take alternate tiles; a group is 8 warps, two per TMEM lane quarter, each
+// owning 64 of the tile's 128 columns.  Then TMA producer, MMA1 issuer, MMA2 issuer.
+constexpr int kGroups = 2;
+constexpr int kGroupWarps = 8;
+constexpr int kEpiWarps = kGroups * kGroupWarps;
+constexpr int kColsPerWarp = kBN / 2;
+constexpr int kWarpTma = kEpiWarps, kWarpMma1 = kEpiWarps + 1, kWarpMma2 = kEpiWarps + 2;
+constexpr int kIterThreads = (kEpiWarps + 3) * 32;
 
 template <int DP>
 struct IterCfg {
@@ -65,19 +69,27 @@ struct IterCfg {
   static constexpr int SMEM = 1024 /*align slack*/ + 2 * 3 * A_B + STAGES * 2 * TILE_B + GS_B + 1024 /*barriers*/;
 };
 
-// in-window weights of two pixels -> packed fp16 {0, 1.0} pair (low half = first pixel)
-__device__ __forceinline__ uint32_t flat_kernel_pair(float c0, float c1, float tau) {
-  const float u0 = c0 - tau, u1 = c1 - tau;  // exact near tau (Sterbenz); sign(u) = [c < tau]
+// In-window weights of two pixels -> packed fp16 pair of {0, 1.75}, low half = first pixel.
+// C and tau are 2^11-scaled fp32 numbers in [1024, 2048) near the threshold, so c - tau_m (tau_m =
+// the float just below tau) is an exact multiple of 2^-13 and
+//     sat(8192 c - 8192 tau_m) = [c >= tau]            (one FFMA.SAT, exact, inclusive: R5)
+// The byte permute takes the top byte of each 1.0f / 0.0f (0x3F / 0x00) over a zero byte: fp16
+// 0x3F00 = 1.75 or 0.  The weighted sums carry the factor 1.75 exactly (see the drain); the FMA
+// pipe does the compare and a single ALU op per pair packs.
+__device__ __forceinline__ uint32_t flat_kernel_pair(float c0, float c1, float k_tau) {
+  const float w0 = __saturatef(__fmaf_rn(c0, 8192.0f, k_tau));
+  const float w1 = __saturatef(__fmaf_rn(c1, 8192.0f, k_tau));
   uint32_t m;
-  asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(m) : "r"(__float_as_uint(u0)), "r"(__float_as_uint(u1)));
-  return ~m & 0x3C003C00u;  // sign-replicated masks select 0 (outside) or 1.0 (inside, c >= tau)
+  asm("prmt.b32 %0, %1, %2, 0x7430;" : "=r"(m) : "r"(__float_as_uint(w0)), "r"(__float_as_uint(w1)));
+  return m;
 }
+constexpr double kPScale = 1.75;  // value of an in-window weight
 
-// Timing experiments (tools/iter_probe.cu): -DFMS_K2_EXPERIMENTS lets Params::variant bits switch
-// parts of the kernel off, -DFMS_K2_TIMELINE logs a clock64 timeline of CTA 0.  The production
+// Timing experiments (tools/iter_probe.cu): -DFMS_K2_VARIANT=bits switches parts of the kernel off
+// (1 weighted-sum MMAs, 2 weight stores, 8/12 similarity MMAs, 16 C loads, 64 pixel loads), -DFMS_K2_TIMELINE logs a clock64 timeline of CTA 0.  The production
 // build compiles both hooks away.
-#ifdef FMS_K2_EXPERIMENTS
-#define K2_OFF(p, bit) ((p).variant & (bit))
+#ifdef FMS_K2_VARIANT
+#define K2_OFF(p, bit) (FMS_K2_VARIANT & (bit))
 #else
 #define K2_OFF(p, bit) (0)
 #endif
@@ -139,7 +151,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1);
-      mbar_init(&g_full[i], 1); mbar_init(&g_empty[i], kGroupWarps);
+      mbar_init(&g_full[i], 1); mbar_init(&g_empty[i], 4);  // drained by 4 warps (one per quarter)
     }
     // epilogue barriers take one arrive per warp (after __syncwarp): 256 same-address arrives
     // per tile would serialise in the shared-memory atomic unit
@@ -148,16 +160,16 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     fence_barrier_init();
     fence_proxy_async();
   }
-  if (warp == 0 && lane == 0) {
+  if (warp == kWarpTma && lane == 0) {
     tma_prefetch(&tm.xh); tma_prefetch(&tm.xl);
     tma_prefetch(&tm.sh); tma_prefetch(&tm.ss); tma_prefetch(&tm.sl);
   }
-  if (warp == 1) tmem_alloc(tmem_holder, 512);
+  if (warp == kWarpMma1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  if (warp == 0) {
+  if (warp == kWarpTma) {
     // ================================ TMA producer ================================
     int xi = 0;
     int stage = 0;
@@ -197,7 +209,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         if (++stage == Cfg::STAGES) { stage = 0; sphase ^= 1; }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kWarpMma1) {
     // ============================ MMA1 issuer: similarity ============================
     // C[i % NC] = 2^11 S.X^T for every tile of the CTA's stream; a C buffer is rewritten as soon as
     // the epilogue has loaded the previous tile from it (c_empty).
@@ -247,7 +259,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
       }
       tc_commit_el(&a_empty[ab]);  // seed tile free once this item's MMA1s complete
     }
-  } else if (warp == 2) {
+  } else if (warp == kWarpMma2) {
     // ========================== MMA2 issuer: weighted sum ==========================
     // G[ab] += P[i % NP] . [hi | lo] once the epilogue group has written the weights (p_full); one
     // commit frees the pixel stage and with it the weight buffer (x_empty); at the end of an item
@@ -280,21 +292,23 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
       tc_commit_el(&g_full[ab]);
     }
   } else {
-    // ================================ epilogue (warps 3..10) ================================
-    // Two groups of 4 warps (one warp per TMEM lane quarter); group g handles the tiles with
-    // index % 2 == g out of C buffer g, so each group has two tile periods to hide its TMEM and
-    // barrier latencies.
+    // ================================ epilogue (warps 0..15) ================================
+    // Group g handles the tiles with index % 2 == g out of C buffer g; warp (q, h) of the group
+    // reads lane quarter q, columns [64 h, 64 h + 64) -- half a row, so 64 registers of C.
     const int q = warp & 3;                           // TMEM lane quarter this warp may access
-    const int grp = (warp - kEpiWarp0) >> 2;          // 0 or 1
+    const int h = (warp >> 2) & 1;                    // column half
+    const int grp = warp >> 3;
+    const bool drainer = grp == 0 && h == 0;          // drains G for its quarter
     const int row = q * 32 + lane;                    // seed row within the tile
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    const float tau = p.tau_f * kLimb;                // C is scaled by 2^11 (exact power-of-two scaling)
-    const uint32_t cbase = tmem + lane_base + grp * kBN;
+    // C is scaled by 2^11 (exact); k_tau = -8192 tau_m, tau_m = the float just below 2^11 tau
+    const float k_tau = -8192.0f * __uint_as_float(__float_as_uint(p.tau_f * kLimb) - 1u);
+    const uint32_t cbase = tmem + lane_base + grp * kBN + h * kColsPerWarp;
     uint32_t ctile = 0;                               // running tile index over the CTA's stream
     uint32_t mine = 0;                                // tiles handled by this group so far
     int it = 0;
     double* gs = gsm + row;                           // segment sum of 2^11 G, [k][kBM] (conflict-free)
-    if (grp == 0) {
+    if (drainer) {
 #pragma unroll
       for (int k = 0; k < DP; ++k) gs[k * kBM] = 0.0;
     }
@@ -327,7 +341,9 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         double* dst = p.gacc + ((size_t)w.f * p.S_pad + (size_t)w.tile * kBM + row) * DP;
 #pragma unroll
         for (int k = 0; k < DP; ++k) {
-          if (gs[k * kBM] != 0.0) atomicAdd(dst + k, gs[k * kBM]);
+          // sums of weights 1.75 times integers (multiples of 2^-11) are exact in fp64, and dividing
+          // an exact multiple of 1.75 by 1.75 is exact (correctly rounded, representable quotient)
+          if (gs[k * kBM] != 0.0) atomicAdd(dst + k, gs[k * kBM] / kPScale);
           gs[k * kBM] = 0.0;
         }
       }
@@ -338,47 +354,42 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
       const int ccnt = min(kChunkTiles, p.n_ptiles - w.chunk * kChunkTiles);
       for (int j = 0; j < ccnt; ++j, ++ctile) {
         if ((int)(ctile & 1) != grp) continue;
-        const int lrole = 3 + grp * 4 + q;  // warp-specific timeline role
+        const int lrole = h ? 15 : 3 + grp * 4 + q;  // timeline: the h == 0 warps
         tlog(p, lrole, ctile, 0);
         mbar_wait(&c_full[grp], mine & 1);
         tlog(p, lrole, ctile, 1);
         const uint32_t pb = ctile % Cfg::NP;
         tc_fence_after();
-        // the whole 128-column row in one go: C goes back to MMA1 after a single load latency
-        uint32_t v[kBN];
+        uint32_t v[kColsPerWarp];
         if (!K2_OFF(p, 16)) {
-          tmem_ld128(cbase, v);
+          tmem_ld64(cbase, v);  // one instruction: the scheduler cannot interleave math between pieces
           tmem_ld_wait();
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&c_empty[grp]);  // MMA1 may overwrite C[grp]
         tlog(p, lrole, ctile, 2);
-        uint32_t pk[kBN / 2];
+        // P[pb] is free once the weighted sum of the tile that used it last has completed: probe
+        // now, use the answer after the flat kernel
+        const uint32_t u = ctile - Cfg::NP;
+        const bool need_free = w.mode == 0 && ctile >= (uint32_t)Cfg::NP;
+        bool p_free = !need_free || mbar_test(&x_empty[u % Cfg::STAGES], (u / Cfg::STAGES) & 1);
+        uint32_t pk[kColsPerWarp / 2];
 #pragma unroll
-        for (int i = 0; i < kBN / 2; ++i)
-          pk[i] = flat_kernel_pair(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]), tau);
+        for (int i = 0; i < kColsPerWarp / 2; ++i)
+          pk[i] = flat_kernel_pair(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]), k_tau);
         tlog(p, lrole, ctile, 5);
-        // P[pb] is free once the weighted sum of the tile that used it last has completed
-        if (w.mode == 0 && ctile >= (uint32_t)Cfg::NP) {
-          const uint32_t u = ctile - Cfg::NP;
-          mbar_wait(&x_empty[u % Cfg::STAGES], (u / Cfg::STAGES) & 1);
-          tc_fence_after();
-        }
+        if (!p_free) mbar_wait(&x_empty[u % Cfg::STAGES], (u / Cfg::STAGES) & 1);
         tlog(p, lrole, ctile, 6);
         if (w.mode == 0) {
-          if (!K2_OFF(p, 2)) {
-            const uint32_t pq = tmem + lane_base + Cfg::P_COL + pb * (kBN / 2);
-            tmem_st32(pq, *reinterpret_cast<const uint32_t(*)[32]>(pk));
-            tmem_st32(pq + 32, *reinterpret_cast<const uint32_t(*)[32]>(pk + 32));
-          }
+          tc_fence_after();
+          if (!K2_OFF(p, 2))
+            tmem_st32(tmem + lane_base + Cfg::P_COL + pb * (kBN / 2) + h * (kColsPerWarp / 2),
+                      *reinterpret_cast<const uint32_t(*)[32]>(pk));
           tmem_st_wait();
         } else {
-          __half2 acc = __float2half2_rn(0.f);
 #pragma unroll
-          for (int i = 0; i < kBN / 2; ++i) acc = __hadd2(acc, *reinterpret_cast<const __half2*>(&pk[i]));
-          const float2 a2 = __half22float2(acc);  // exact: <= 64 per half per tile
-          cnt += (int)(a2.x + a2.y);
+          for (int i = 0; i < kColsPerWarp / 2; ++i) cnt += __popc(pk[i] & 0x01000100u);  // bit 8 of 0x3F00
         }
         tlog(p, lrole, ctile, 3);
         tc_fence_before();
@@ -386,9 +397,9 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         if (lane == 0) mbar_arrive(&p_full[pb]);  // MMA2 may consume P[pb]
         tlog(p, lrole, ctile, 4);
         ++mine;
-        if (grp == 0 && pend >= 0) { drain(pend, pend_it); pend = -1; }
+        if (drainer && pend >= 0) { drain(pend, pend_it); pend = -1; }
       }
-      if (grp == 0) {
+      if (drainer) {
         if (pend >= 0) drain(pend, pend_it);
         pend = item;
         pend_it = it;
@@ -400,13 +411,13 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         cnt = 0;
       }
     }
-    if (grp == 0 && pend >= 0) drain(pend, pend_it);
+    if (drainer && pend >= 0) drain(pend, pend_it);
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (warp == kWarpMma1) tmem_dealloc(tmem, 512);
 }
 
 int iter_smem_bytes(int DP) { return DP == 16 ? IterCfg<16>::SMEM : IterCfg<32>::SMEM; }

@@ -65,6 +65,27 @@ __global__ void probe(int reps, unsigned long long* out) {
   if (warp == 0) tmem_dealloc(holder, 512);
 }
 
+// cost of waiting on / probing an already-completed phase
+__global__ void done_wait(int reps, unsigned long long* out) {
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); mbar_arrive(&bar); }
+  __syncthreads();
+  unsigned long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) mbar_wait(&bar, 0);
+  unsigned long long t1 = clock64();
+  int acc = 0;
+  for (int r = 0; r < reps; ++r) acc += mbar_test(&bar, 0);
+  unsigned long long t2 = clock64();
+  uint32_t x = 0;
+  for (int r = 0; r < reps; ++r) { mbar_wait(&bar, 0); x = x * 3 + r; }
+  unsigned long long t3 = clock64();
+  if (threadIdx.x == 0) {
+    out[blockIdx.x * 4 + 0] = (t1 - t0) / reps;
+    out[blockIdx.x * 4 + 1] = (t2 - t1) / reps;
+    out[blockIdx.x * 4 + 2] = acc + (x == 7);
+  }
+}
+
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 64);
@@ -76,5 +97,14 @@ int main() {
   cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
   printf("commit(no MMA)+wait: %llu cycles\narrive+wait same warp: %llu cycles\nMMA128x128x16+commit+wait: %llu cycles\n"
          "cross-warp round trip (2 handoffs): %llu cycles\n", h[0], h[1], h[2], h[3]);
+  {
+    unsigned long long* d;
+    cudaMalloc(&d, 8 * 4 * 148);
+    unsigned long long h[4 * 148];
+    for (int it = 0; it < 2; ++it) done_wait<<<148, 32>>>(256, d);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    printf("completed phase: try_wait loop %llu cyc/wait, test_wait %llu cyc/probe\n", h[0], h[1]);
+  }
   return 0;
 }
