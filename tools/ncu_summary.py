@@ -68,6 +68,10 @@ def full(src, dst, idx=0):
         "sm_cycles_elapsed_avg": f("sm__cycles_elapsed.avg"),
         "tensor_pipe_active_pct_of_peak_elapsed":
             f("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
+        "tensor_pipe_cycles_active_pct_of_peak_elapsed": f("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+        "fp16_tensor_ops_pct_of_peak_elapsed": f("sm__ops_path_tensor_src_fp16_dst_fp32.avg.pct_of_peak_sustained_elapsed"),
+        "issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+        "l2_hit_rate_pct": f("lts__t_sector_hit_rate.pct"),
         "registers_per_thread": f("launch__registers_per_thread"),
         "threads_per_block": f("launch__block_size"),
         "source": src,
