@@ -1,0 +1,329 @@
+// k_assign.cu -- K5 on 5th-generation tensor cores: nearest-centre labels and window coverage.
+//
+// Alg. 2 l.12-14: every pixel takes the label of its most similar mode,
+//     label = argmax_k x_hat . c_k   (lowest k on ties, R21)
+//     covered = max_k x_hat . c_k >= tau   (inside some mode's window, Eq. 11 / R5)
+// plus the per-centre histogram and the count of uncovered & unvisited pixels OSOP needs (K7).
+//
+// The similarity block is the transpose of K2's: D[pixel][centre] = X_hat . C^T with the pixel
+// tile as A (M = 128 pixels, the fp16 limb tiles K2 streams, K-major) and the frame's centres as B
+// (N = Kc rounded up to 16, at most 128), with the same three-term split as K2:
+//     2^11 D = hi.c_hi + lo.(c_hi 2^-11) + hi.c_lo      (fp32 accumulate, ~1e-7 error)
+// so coverage takes exactly K2's window decision [2^11 x.c >= 2^11 tau] (fp32).  One TMEM lane
+// per pixel turns the row argmax into a per-thread scan of Kc registers.
+//
+//   * warp 0   : TMA producer of pixel tiles (hi, lo); converts the frame's centres to the fp16
+//                split on the fly and stores them into shared memory in the K-major swizzled layout
+//                the MMA descriptor expects (double buffered by frame).
+//   * warp 1   : MMA issuer, D[i % 4] (128 TMEM columns each).
+//   * warps 2-17: four groups of 4 warps (one per TMEM lane quarter) take the tiles round robin;
+//                the per-pixel argmax is a dependent scan, so it needs the thread parallelism.
+// Frames with more than 128 centres are left to the CUDA-core kernel (assign_kernel in k_post.cu).
+#include "fms_device.cuh"
+
+namespace fms {
+
+constexpr int kAsgMaxN = 128;     // centres per frame handled here (one MMA N)
+constexpr int kAsgGroups = 4;     // epilogue groups (tile mod 4), one TMEM buffer of 128 columns each
+constexpr int kAsgEpiWarp0 = 2;
+constexpr int kAsgEpiThreads = kAsgGroups * 4 * 32;
+constexpr int kAsgThreads = kAsgEpiWarp0 * 32 + kAsgEpiThreads;
+
+template <int DP>
+struct AsgCfg {
+  static constexpr int ROW_B = DP * 2;
+  static constexpr int TILE_B = kBN * ROW_B;              // one pixel tile, one limb
+  static constexpr int CEN_B = kAsgMaxN * ROW_B;          // one centre split
+  static constexpr uint32_t LAYOUT = DP == 16 ? 6u : 4u;  // SWIZZLE_32B / SWIZZLE_64B
+  static constexpr uint32_t SBO = 8 * ROW_B;
+  static constexpr int STAGES = DP == 16 ? 8 : 5;
+  static constexpr int SMEM = 1024 + 2 * 3 * CEN_B + STAGES * 2 * TILE_B + 2 * kAsgMaxN * 4 + 1024;
+};
+
+// byte offset of (row, 16-byte chunk) in a K-major tile with 32-byte (SW32) / 64-byte (SW64)
+// swizzled rows -- the layout TMA writes for the pixel tiles (16-byte chunk index XOR row bits)
+template <int DP>
+__device__ __forceinline__ uint32_t swz_off(int row, int chunk) {
+  if constexpr (DP == 16) return row * 32 + ((chunk ^ ((row >> 2) & 1)) << 4);
+  else return row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4);
+}
+
+__device__ __forceinline__ bool asg_frame_active(const Params& p, int f) {
+  const FrameCtl& c = p.ctl[f];
+  return c.phase == PH_POST && c.Kc > 0 && c.Kc <= kAsgMaxN;
+}
+
+template <int DP>
+__global__ void __launch_bounds__(kAsgThreads, 1) assign_tc_kernel(const __grid_constant__ TMaps tm, Params p) {
+  using Cfg = AsgCfg<DP>;
+  const long long n_items = (long long)p.B * p.n_ptiles;
+  const int i_begin = (int)((n_items * blockIdx.x) / gridDim.x);
+  const int i_end = (int)((n_items * (blockIdx.x + 1)) / gridDim.x);
+  if (i_begin >= i_end) return;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sC = smem;                                   // [2 frames][hi, hs, lo][CEN_B]
+  uint8_t* sX = sC + 2 * 3 * Cfg::CEN_B;                // [STAGES][hi, lo][TILE_B]
+  int* shist = reinterpret_cast<int*>(sX + Cfg::STAGES * 2 * Cfg::TILE_B);  // [2][kAsgMaxN]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(shist + 2 * kAsgMaxN);
+  uint64_t* x_full = bars;                   // [STAGES]
+  uint64_t* x_empty = x_full + Cfg::STAGES;  // [STAGES]
+  uint64_t* c_full = x_empty + Cfg::STAGES;  // [2] centres of a frame staged
+  uint64_t* c_empty = c_full + 2;            // [2] last MMA of that frame done
+  uint64_t* d_full = c_empty + 2;            // [kAsgGroups] similarity block ready
+  uint64_t* d_empty = d_full + kAsgGroups;   // [kAsgGroups] loaded by the epilogue group
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(d_empty + kAsgGroups);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&c_full[i], 32); mbar_init(&c_empty[i], 1); }
+    for (int i = 0; i < kAsgGroups; ++i) { mbar_init(&d_full[i], 1); mbar_init(&d_empty[i], 4); }
+    fence_barrier_init();
+    fence_proxy_async();
+  }
+  for (int i = threadIdx.x; i < 2 * kAsgMaxN; i += blockDim.x) shist[i] = 0;
+  if (warp == 1) tmem_alloc(tmem_holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    // ================================ producer ================================
+    int stage = 0, fcount = 0, last_f = -1, act_f = -1;
+    bool act_v = false;
+    uint32_t sphase = 0;
+    for (int item = i_begin, f = i_begin / p.n_ptiles, t = i_begin - f * p.n_ptiles; item < i_end;
+         ++item, t = (t + 1 == p.n_ptiles) ? (++f, 0) : t + 1) {
+      if (f != act_f) { act_f = f; act_v = asg_frame_active(p, f); }
+      if (!act_v) continue;
+      if (f != last_f) {
+        // stage this frame's centre split into buffer fcount & 1 once its previous user is done
+        const int cb = fcount & 1;
+        mbar_wait(&c_empty[cb], ((fcount >> 1) & 1) ^ 1);
+        const int Kc = p.ctl[f].Kc;
+        const float* cent = p.cent + (size_t)f * p.C_cap * DP;
+        uint8_t* dst = sC + cb * 3 * Cfg::CEN_B;
+        const int n_rows = (Kc + 15) & ~15;
+        for (int idx = lane; idx < n_rows * (DP / 8); idx += 32) {  // one 8-feature chunk per step
+          const int r = idx / (DP / 8), ch = idx - r * (DP / 8);
+          __align__(16) __half hi[8], hs[8], lo[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float v = r < Kc ? cent[(size_t)r * DP + ch * 8 + e] : 0.f;
+            split_seed(v, hi[e], hs[e], lo[e]);
+          }
+          const uint32_t off = swz_off<DP>(r, ch);
+          *reinterpret_cast<uint4*>(dst + off) = *reinterpret_cast<const uint4*>(hi);
+          *reinterpret_cast<uint4*>(dst + Cfg::CEN_B + off) = *reinterpret_cast<const uint4*>(hs);
+          *reinterpret_cast<uint4*>(dst + 2 * Cfg::CEN_B + off) = *reinterpret_cast<const uint4*>(lo);
+        }
+        fence_proxy_async();  // generic-proxy stores -> visible to the tensor core
+        mbar_arrive(&c_full[cb]);
+        last_f = f;
+        ++fcount;
+      }
+      mbar_wait(&x_empty[stage], sphase ^ 1);
+      if (lane == 0) {
+        const int xrow = (int)((long long)f * p.n_pad + (long long)t * kBN);
+        mbar_expect_tx(&x_full[stage], 2 * Cfg::TILE_B);
+        tma_load_2d(sX + (2 * stage) * Cfg::TILE_B, &tm.xh, &x_full[stage], 0, xrow);
+        tma_load_2d(sX + (2 * stage + 1) * Cfg::TILE_B, &tm.xl, &x_full[stage], 0, xrow);
+      }
+      __syncwarp();
+      if (++stage == Cfg::STAGES) { stage = 0; sphase ^= 1; }
+    }
+  } else if (warp == 1) {
+    // ================================ MMA issuer ================================
+    // A = pixel tile (M = 128, K-major), B = centres (N = Kc rounded to 16, K-major)
+    const uint64_t dx0 = umma_desc(smem_u32(sX), 16, Cfg::SBO, Cfg::LAYOUT);
+    const uint64_t dc0 = umma_desc(smem_u32(sC), 16, Cfg::SBO, Cfg::LAYOUT);
+    int stage = 0, fcount = 0, last_f = -1, i = 0, act_f = -1;
+    bool act_v = false;
+    uint32_t sphase = 0;
+    uint32_t idesc = 0;
+    uint64_t dch = 0, dcs = 0, dcl = 0;
+    for (int item = i_begin, f = i_begin / p.n_ptiles, t = i_begin - f * p.n_ptiles; item < i_end;
+         ++item, t = (t + 1 == p.n_ptiles) ? (++f, 0) : t + 1) {
+      if (f != act_f) { act_f = f; act_v = asg_frame_active(p, f); }
+      if (!act_v) continue;
+      if (f != last_f) {
+        if (last_f >= 0) tc_commit_el(&c_empty[(fcount - 1) & 1]);  // previous frame's centres free
+        const int cb = fcount & 1;
+        mbar_wait(&c_full[cb], (fcount >> 1) & 1);
+        tc_fence_after();
+        const int nN = (p.ctl[f].Kc + 15) & ~15;
+        idesc = idesc_f16(kBM, nN, 0, 0);
+        dch = dc0 + (uint64_t)((cb * 3 * Cfg::CEN_B) >> 4);
+        dcs = dch + (Cfg::CEN_B >> 4);
+        dcl = dch + (2 * Cfg::CEN_B >> 4);
+        last_f = f;
+        ++fcount;
+      }
+      const uint32_t db = i % kAsgGroups;
+      if (i >= kAsgGroups) mbar_wait(&d_empty[db], ((i / kAsgGroups) - 1) & 1);
+      mbar_wait(&x_full[stage], sphase);
+      tc_fence_after();
+      const uint64_t dxh = dx0 + (uint64_t)(stage * (2 * Cfg::TILE_B >> 4));
+      const uint64_t dxl = dxh + (Cfg::TILE_B >> 4);
+      const uint32_t d = tmem + db * kAsgMaxN;
+#pragma unroll
+      for (int kk = 0; kk < DP / 16; ++kk) mma_ss_f16_el(d, dxh + kk * 2, dch + kk * 2, idesc, kk > 0);  // hi.c_hi
+#pragma unroll
+      for (int kk = 0; kk < DP / 16; ++kk) mma_ss_f16_el(d, dxl + kk * 2, dcs + kk * 2, idesc, 1u);  // lo.c_hs
+#pragma unroll
+      for (int kk = 0; kk < DP / 16; ++kk) mma_ss_f16_el(d, dxh + kk * 2, dcl + kk * 2, idesc, 1u);  // hi.c_lo
+      tc_commit_el(&d_full[db]);
+      tc_commit_el(&x_empty[stage]);
+      ++i;
+      if (++stage == Cfg::STAGES) { stage = 0; sphase ^= 1; }
+    }
+    if (last_f >= 0) tc_commit_el(&c_empty[(fcount - 1) & 1]);
+  } else {
+    // ================================ epilogue ================================
+    const int q = warp & 3;
+    const int grp = (warp - kAsgEpiWarp0) >> 2;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const float tau2 = p.tau_f * kLimb;  // D is 2^11-scaled
+    int i = 0, last_f = -1, fcount = 0;
+    int cand = 0;
+    auto flush = [&](int f, int hb) {  // per-frame histogram and candidate count -> global
+      asm volatile("bar.sync 1, %0;" ::"n"(kAsgEpiThreads) : "memory");  // the epilogue warps
+      int* hs = shist + hb * kAsgMaxN;
+      const int Kc = p.ctl[f].Kc;
+      for (int k = threadIdx.x - kAsgEpiWarp0 * 32; k < Kc; k += kAsgEpiThreads) {
+        if (hs[k]) atomicAdd(&p.hist[(size_t)f * p.C_cap + k], hs[k]);
+        hs[k] = 0;
+      }
+      const int tot = __reduce_add_sync(0xffffffffu, cand);
+      if (lane == 0 && tot) atomicAdd((unsigned long long*)&p.ctl[f].ncand, (unsigned long long)tot);
+      cand = 0;
+      asm volatile("bar.sync 1, %0;" ::"n"(kAsgEpiThreads) : "memory");
+    };
+    // Items are walked with an incremental (frame, tile) cursor: a division per item would cost
+    // more than the tile's argmax.
+    struct Cur {
+      int item, f, t;
+    };
+    auto step = [&](Cur& c) {
+      ++c.item;
+      if (++c.t == p.n_ptiles) { c.t = 0; ++c.f; }
+    };
+    int act_f = -1;
+    bool act_v = false;
+    auto active = [&](int f) -> bool {  // frame-active test, cached (frames change rarely)
+      if (f != act_f) { act_f = f; act_v = asg_frame_active(p, f); }
+      return act_v;
+    };
+    auto flag_of = [&](const Cur& c) -> uint8_t {
+      const long long px = (long long)c.t * kBN + q * 32 + lane;
+      return px < p.n ? p.flags[(size_t)c.f * p.n + px] : 0;
+    };
+    // this group's next tile: the kAsgGroups-th active item after c
+    auto next_mine = [&](Cur c) -> Cur {
+      for (int k = 0; k < kAsgGroups;) {
+        step(c);
+        if (c.item >= i_end) return c;
+        if (active(c.f)) ++k;
+      }
+      return c;
+    };
+    const Cur c0{i_begin, i_begin / p.n_ptiles, i_begin - (i_begin / p.n_ptiles) * p.n_ptiles};
+    Cur pf = c0;  // first tile of this group: the (grp+1)-th active item
+    for (int k = 0; pf.item < i_end; step(pf)) {
+      if (!active(pf.f)) continue;
+      if (k++ == grp) break;
+    }
+    uint8_t pf_flag = pf.item < i_end ? flag_of(pf) : 0;
+    for (Cur c = c0; c.item < i_end; step(c)) {
+      const int f = c.f, t = c.t;
+      if (!active(f)) continue;
+      if (f != last_f) {
+        if (last_f >= 0) flush(last_f, (fcount - 1) & 1);
+        last_f = f;
+        ++fcount;
+      }
+      const int my = i;
+      ++i;
+      if (my % kAsgGroups != grp) continue;
+      // The pixel flags come from global memory; the read for the group's next tile is issued
+      // now, so its latency overlaps this tile.
+      const uint8_t fl = pf_flag;  // pf == c
+      pf = next_mine(c);
+      if (pf.item < i_end) pf_flag = flag_of(pf);
+      const uint32_t db = my % kAsgGroups;
+      const int Kc = p.ctl[f].Kc;
+      mbar_wait(&d_full[db], (my / kAsgGroups) & 1);
+      tc_fence_after();
+      // argmax over the row in four interleaved streams (short dependency chains); each stream
+      // keeps its first maximum, the merge prefers the larger value, then the lower index
+      float bv[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      int bl[4] = {0, 1, 2, 3};
+      const uint32_t dbase = tmem + lane_base + db * kAsgMaxN;
+      for (int c0 = 0; c0 < Kc; c0 += 64) {
+        uint32_t v[64];
+        tmem_ld64(dbase + c0, v);
+        tmem_ld_wait();
+        if (Kc - c0 >= 64) {
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            const float dv = __uint_as_float(v[k]);
+            if (dv > bv[k & 3]) { bv[k & 3] = dv; bl[k & 3] = c0 + k; }
+          }
+        } else {
+          const int nk = Kc - c0;
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            const float dv = k < nk ? __uint_as_float(v[k]) : -INFINITY;
+            if (dv > bv[k & 3]) { bv[k & 3] = dv; bl[k & 3] = c0 + k; }
+          }
+        }
+      }
+      float best = bv[0];
+      int lab = bl[0];
+#pragma unroll
+      for (int s2 = 1; s2 < 4; ++s2)
+        if (bv[s2] > best || (bv[s2] == best && bl[s2] < lab)) { best = bv[s2]; lab = bl[s2]; }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&d_empty[db]);
+      const long long px = (long long)t * kBN + q * 32 + lane;
+      if (px < p.n) {
+        const size_t pi = (size_t)f * p.n + px;
+        const bool covered = best >= tau2;
+        p.flags[pi] = (uint8_t)((fl & ~PF_COVERED) | (covered ? PF_COVERED : 0));
+        p.labels[pi] = lab;
+        // warp-aggregated histogram: neighbouring pixels mostly share a label, and 32 same-address
+        // shared atomics would serialise
+        const unsigned same = __match_any_sync(__activemask(), lab);
+        if ((__ffs(same) - 1) == lane) atomicAdd(&shist[((fcount - 1) & 1) * kAsgMaxN + lab], __popc(same));
+        cand += (!covered && !(fl & PF_VISITED)) ? 1 : 0;
+      }
+    }
+    if (last_f >= 0) flush(last_f, (fcount - 1) & 1);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+int assign_tc_smem_bytes(int DP) { return DP == 16 ? AsgCfg<16>::SMEM : AsgCfg<32>::SMEM; }
+
+cudaError_t setup_assign_attrs() {
+  cudaError_t e = cudaFuncSetAttribute(assign_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, AsgCfg<16>::SMEM);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(assign_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, AsgCfg<32>::SMEM);
+}
+
+cudaError_t launch_assign_tc(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st) {
+  if (DP == 16) assign_tc_kernel<16><<<grid, kAsgThreads, AsgCfg<16>::SMEM, st>>>(tm, p);
+  else assign_tc_kernel<32><<<grid, kAsgThreads, AsgCfg<32>::SMEM, st>>>(tm, p);
+  return cudaGetLastError();
+}
+
+}  // namespace fms

@@ -8,7 +8,8 @@
 //     chain resolved by one warp with ballots).
 // K5 (Alg. 2 l.12-14): label = argmax_k x.c_k (lowest k on ties, R21); covered =
 //     max_k x_hat.c_k >= tau; per-centre histogram; count of uncovered & unvisited pixels.
-//     fp32 FMA on the fp32 input (HBM-bound scan; full-precision decisions for coverage).
+//     Frames with <= 128 centres run on the tensor cores (k_assign.cu); this fp32 CUDA-core scan
+//     of the input covers frames with more centres.
 // K7 (Eq. 12-19; readings R12-R15, R22): background = largest cluster,
 //     I = #other clusters with >= min_instance_px pixels, r = 1 - |bg|/n,
 //     N_min = ceil( ln(1 - e^{ln P / I}) / ln(1 - r/I) ); stop when coverage holds
@@ -165,14 +166,18 @@ __global__ void __launch_bounds__(1024) merge_kernel(Params p) {
 template <int DP>
 __global__ void __launch_bounds__(256) assign_kernel(Params p) {
   constexpr int kAsgChunk = 8192 / DP;  // centres per SMEM chunk (32 KB)
-  const int f = blockIdx.y;
-  FrameCtl& c = p.ctl[f];
-  if (c.phase != PH_POST) return;
   __shared__ float sc[kAsgChunk * DP];
   __shared__ int sh[kAsgChunk];
   __shared__ int s_cand;
+  // grid (16, B): most frames go to assign_tc_kernel and their CTAs exit at once; the others are
+  // covered by a block-stride loop over 256-pixel blocks
+  const int f = blockIdx.y;
+  FrameCtl& c = p.ctl[f];
+  if (c.phase != PH_POST || (c.Kc > 0 && c.Kc <= 128)) return;  // <= 128 centres: assign_tc_kernel
+  const int nb = (int)((p.n + 255) / 256);
+  for (int bid = blockIdx.x; bid < nb; bid += gridDim.x) {
   const int Kc = c.Kc;
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long i = (long long)bid * blockDim.x + threadIdx.x;
   const bool valid = i < p.n;
   float x[DP];
 #pragma unroll
@@ -219,6 +224,7 @@ __global__ void __launch_bounds__(256) assign_kernel(Params p) {
   }
   cand = __syncthreads_count(cand);
   if (threadIdx.x == 0 && cand) atomicAdd((unsigned long long*)&c.ncand, (unsigned long long)cand);
+  }
 }
 
 __global__ void osop_kernel(Params p) {
@@ -305,16 +311,17 @@ cudaError_t setup_post_attrs(int P_cap) {
                               merge_smem_bytes(P_cap, 32));
 }
 
-cudaError_t launch_post(const Params& p, cudaStream_t st) {
+cudaError_t launch_assign_tc(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st);
+
+cudaError_t launch_post(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st) {
   const int sm = merge_smem_bytes(p.P_cap, p.DP);
-  dim3 ga((unsigned)((p.n + 255) / 256), p.B);
-  if (p.DP == 16) {
-    merge_kernel<16><<<p.B, 1024, sm, st>>>(p);
-    assign_kernel<16><<<ga, 256, 0, st>>>(p);
-  } else {
-    merge_kernel<32><<<p.B, 1024, sm, st>>>(p);
-    assign_kernel<32><<<ga, 256, 0, st>>>(p);
-  }
+  const dim3 ga(16, p.B);
+  if (p.DP == 16) merge_kernel<16><<<p.B, 1024, sm, st>>>(p);
+  else merge_kernel<32><<<p.B, 1024, sm, st>>>(p);
+  cudaError_t e = launch_assign_tc(p.DP, tm, p, num_sms, st);  // frames with <= 128 centres
+  if (e != cudaSuccess) return e;
+  if (p.DP == 16) assign_kernel<16><<<ga, 256, 0, st>>>(p);    // the rest
+  else assign_kernel<32><<<ga, 256, 0, st>>>(p);
   osop_kernel<<<1, 1024, 0, st>>>(p);
   return cudaGetLastError();
 }

@@ -30,7 +30,8 @@ cudaError_t launch_select(const Params& p, int num_sms, cudaStream_t st);
 cudaError_t launch_plan(const Params& p, cudaStream_t st);
 cudaError_t launch_iter(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st);
 cudaError_t launch_update_ctl(const Params& p, int num_sms, cudaStream_t st);
-cudaError_t launch_post(const Params& p, cudaStream_t st);
+cudaError_t launch_post(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st);
+cudaError_t setup_assign_attrs();
 cudaError_t launch_output(const Params& p, float* centres_out, int cap, cudaStream_t st);
 cudaError_t setup_iter_attrs();
 cudaError_t setup_post_attrs(int P_cap);
@@ -170,6 +171,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   CU(cudaSetDevice(c->device));
   if (!c->attrs_done) {
     CU(setup_iter_attrs());
+    CU(setup_assign_attrs());
     CU(setup_post_attrs(kMaxPcap));
     CU(cudaEventCreate(&c->t0));
     CU(cudaEventCreate(&c->t1));
@@ -300,8 +302,8 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
       if (c->h_counters[5]) return fail(c, FMS_E_INTERNAL, "work-item capacity exceeded");
       if (c->h_counters[3] == 0) break;  // no frame still iterating
     }
-    CU(launch_post(p, st));
-    kernels += 3;
+    CU(launch_post(p, tm, c->num_sms, st));
+    kernels += 4;  // merge, assign (tensor cores), assign (CUDA cores, > 256 centres), osop
     CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (c->h_counters[2] == 0) break;  // every frame DONE (or in error)
