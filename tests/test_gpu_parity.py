@@ -121,6 +121,34 @@ def test_c3_nonsquare_ari():
     check_near(f.emb, rng_seed=0, min_instance_px=min_instance_px(f.n), saturation_stop=1)
 
 
+def _many_clusters(k=200, per=80, d=16, seed=7):
+    """k well-separated directions (pairwise cosine < 0.7), `per` pixels each within cosine 0.97."""
+    rng = np.random.default_rng(seed)
+    dirs = []
+    while len(dirs) < k:
+        v = rng.standard_normal(d)
+        v /= np.linalg.norm(v)
+        if all(abs(float(v @ u)) < 0.7 for u in dirs):
+            dirs.append(v)
+    dirs = np.array(dirs)
+    pts = []
+    for c in range(k):
+        noise = rng.standard_normal((per, d)) * 0.04
+        x = dirs[c] + noise
+        x /= np.linalg.norm(x, axis=1, keepdims=True)
+        pts.append(x)
+    emb = np.concatenate(pts)[rng.permutation(k * per)]
+    return emb.astype(np.float32)
+
+
+def test_more_than_128_modes_exact():
+    """> 128 modes: the last rounds' assignment runs on the CUDA-core kernel, earlier ones on the
+    tensor cores -- both must reproduce the oracle exactly (Alg. 2 l.12-14)."""
+    emb = _many_clusters()
+    lg, cg, Kg, st, ro = check_exact(emb, rng_seed=3, has_background=0)
+    assert ro.K > 128 and max(ro.trace["round_Kc"]) > 128
+
+
 # ---------------------------------------------------------------------------------------------
 # batching, determinism, host entry
 # ---------------------------------------------------------------------------------------------
