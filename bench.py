@@ -38,6 +38,12 @@ def parse():
     ap.add_argument("--config", default=CONFIG)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", default="replicas", choices=["replicas", "seeds"],
+                    help="replicas: every rank clusters its own frames (weak scaling); seeds: every rank "
+                         "clusters the same frames and iterates 1/N of each round's seeds (strong scaling, "
+                         "SURVEY 8(e)2; exchange through torch.distributed)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend of the fms arm (gloo: several ranks may share one GPU)")
     return ap.parse_args()
 
 
@@ -54,8 +60,8 @@ def dist_init(args):
         import torch
         import torch.distributed as dist
         if args.impl == "fms":
-            torch.cuda.set_device(local)
-            dist.init_process_group("nccl")
+            torch.cuda.set_device(local % torch.cuda.device_count())
+            dist.init_process_group(args.backend)
         else:
             dist.init_process_group("gloo")
     return world, rank, local
@@ -113,6 +119,8 @@ def reduce_max(x: float, world: int, device=None) -> float:
         return x
     import torch
     import torch.distributed as dist
+    if dist.get_backend() != "nccl":
+        device = None  # gloo reduces host tensors
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.barrier()
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -188,16 +196,22 @@ def main():
     import paper_2007_14283_b200 as fms
     import synth
 
+    local = local % torch.cuda.device_count()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     B = args.batch
-    # pool of 2 batches (inputs 2 x B x 16 MiB > 126 MB L2 for B >= 4), alternated step to step
-    frames = [synth.make_frame(args.config, 10000 * rank + i) for i in range(2 * B)]
+    sharded = args.shard == "seeds" and world > 1
+    # pool of 2 batches (inputs 2 x B x 16 MiB > 126 MB L2 for B >= 4), alternated step to step;
+    # seed sharding: all ranks work on the same frames
+    frames = [synth.make_frame(args.config, 10000 * (0 if sharded else rank) + i) for i in range(2 * B)]
     n, d = frames[0].n, frames[0].D
     pool = torch.from_numpy(np.stack([f.emb for f in frames])).to(dev).view(2, B, n, d)
     labels = torch.empty((B, n), dtype=torch.int32, device=dev)
     cent = torch.empty((B, CAP, d), dtype=torch.float32, device=dev)
     ctx = fms.context(local)
+    if sharded:
+        from paper_2007_14283_b200.dist import enable_seed_sharding
+        enable_seed_sharding(ctx)
     pol = fms.default_policy(**policy_kwargs(n))
     stream = torch.cuda.current_stream(dev)
 
@@ -228,7 +242,7 @@ def main():
         torch.cuda.synchronize()
     ms = reduce_max(ev0.elapsed_time(ev1), world, dev)
     ctx.set_option("profile_iter", 0)
-    frames_total = totals["frames"] * world
+    frames_total = totals["frames"] * (1 if sharded else world)
     value = frames_total / (ms / 1e3)
 
     # end-to-end through the host-pointer C-ABI entry (H2D + cluster + D2H inside the call)
@@ -249,7 +263,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         ems = reduce_max(e0.elapsed_time(e1), world, dev)
-        e2e = {"value": ksteps * B * world / (ems / 1e3), "unit": "frames/s",
+        e2e = {"value": ksteps * B * (1 if sharded else world) / (ems / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": B * n * d * 4, "d2h_bytes_per_step": B * n * 4 + B * CAP * d * 4}
 
     if rank != 0:
@@ -275,12 +289,13 @@ def main():
     line = {
         "metric": f"frames/sec ({f0.H}x{f0.W}, {d}-D embeddings) and mean-shift iteration % of roofline",
         "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None,
         "dtype": "f16x3 split / f32 accumulate", "data": "synthetic",
         "config": {"workload": f"{args.config}: {f0.H}x{f0.W} frame, {d}-D, {f0.cells} touching/overlapping cells "
                                f"+ background, full OSOP (N_initial 128, gamma 0.9, L 2, P 0.99)",
                    "frames_per_step": B, "l2": "2 alternating input batches of B x 16 MiB (> 126 MB L2)",
-                   "parallelism": f"replicas x{world}"},
+                   "parallelism": f"seed-sharded x{world} ({args.backend})" if sharded else f"replicas x{world}"},
         "roofline": roof,
         "frame_level_frac": frame_roof_ms / ms if ms > 0 else None,
         "seed_iters_per_frame": totals["seed_iters"] / max(1, totals["frames"]),

@@ -95,6 +95,23 @@ void fms_ctx_destroy(void* ctx);
 const char* fms_last_error(const void* ctx);
 const char* fms_version(void);
 
+/* Seed sharding (the seeds of a round are independent mean-shift trajectories,
+ * Alg. 2 l.4-9, so a round's seeds can be split over GPUs that each hold the
+ * whole frame).  With world > 1, rank r iterates only the round seeds j with j % world == r; the
+ * library calls `fn` at two exchange points and expects it to replace the int32 device buffer
+ * `buf[0..count)` by its elementwise sum over all ranks, stream-ordered on `stream` (e.g. an
+ * all-reduce through torch.distributed), returning 0 on success:
+ *   - once per lockstep step: per frame (active, converged, stalled) counts, so the early-stop test
+ *     converged >= ceil(gamma K_r) sees the whole round on every rank;
+ *   - once per round before the merge: every owner's converged seeds (fp32 bits), statuses and
+ *     intensities (non-owners contribute zeros, so the integer sum is exact).
+ * Selection, merge, assignment and OSOP control then run replicated and bit-identical on every rank,
+ * and every rank returns the full result.  All ranks must pass the same frames and parameters.
+ * world = 1 (the default) disables sharding.  Errors: FMS_E_INVALID for rank/world out of range or
+ * a NULL fn with world > 1; a nonzero return of fn makes the clustering call fail with FMS_E_NCCL. */
+typedef int (*fms_exchange_fn)(void* user, int32_t* buf, int64_t count, void* stream);
+fms_status fms_set_exchange(void* ctx, fms_exchange_fn fn, void* user, int32_t rank, int32_t world);
+
 /* Options: "profile_iter" (0/1): time every K2 launch with CUDA events for fms_run_stats.iter_ms. */
 fms_status fms_set_option(void* ctx, const char* key, int64_t value);
 

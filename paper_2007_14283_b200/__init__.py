@@ -15,7 +15,10 @@ MAX_ROUNDS = 16
 STATUS = {0: "OK", 2: "INVALID", 3: "ZERO_NORM", 4: "STALLED", 5: "CAPACITY", 6: "CUDA", 7: "NCCL", 8: "OOM",
           9: "INTERNAL"}
 EXPORTS = ["fms_default_policy", "fms_ctx_create", "fms_ctx_destroy", "fms_last_error", "fms_version",
-           "fms_set_option", "fms_cluster", "fms_cluster_batch", "fms_cluster_batch_host"]
+           "fms_set_option", "fms_set_exchange", "fms_cluster", "fms_cluster_batch", "fms_cluster_batch_host"]
+
+# int (*)(void* user, int32_t* buf, int64_t count, void* stream): in-place int32 sum over ranks
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfms.so")
@@ -77,12 +80,13 @@ def lib() -> C.CDLL:
         L.fms_ctx_destroy.argtypes = [vp]
         L.fms_ctx_destroy.restype = None
         L.fms_set_option.argtypes = [vp, C.c_char_p, i64]
+        L.fms_set_exchange.argtypes = [vp, EXCHANGE_FN, vp, i32, i32]
         common = [f64, i32, f64, C.POINTER(Policy), vp, vp, i32, vp, vp, C.POINTER(RunStats), vp]
         L.fms_cluster.argtypes = [vp, vp, i64, i32] + common
         L.fms_cluster_batch.argtypes = [vp, vp, i32, i64, i32] + common
         L.fms_cluster_batch_host.argtypes = [vp, vp, i32, i64, i32] + common
-        for fn in ("fms_default_policy", "fms_ctx_create", "fms_set_option", "fms_cluster", "fms_cluster_batch",
-                   "fms_cluster_batch_host"):
+        for fn in ("fms_default_policy", "fms_ctx_create", "fms_set_option", "fms_set_exchange", "fms_cluster",
+                   "fms_cluster_batch", "fms_cluster_batch_host"):
             getattr(L, fn).restype = C.c_int
         _lib = L
     return _lib
@@ -126,6 +130,23 @@ class Context:
 
     def set_option(self, key: str, value: int):
         self._check(lib().fms_set_option(self.h, key.encode(), int(value)))
+
+    def set_exchange(self, fn, rank: int, world: int):
+        """Seed sharding (include/fms.h fms_set_exchange).  fn(buf_ptr, count, stream_ptr) must replace
+        the int32 device buffer by its sum over all ranks, ordered on the given stream, and return 0;
+        world = 1 (fn None) turns sharding off.  paper_2007_14283_b200.dist builds fn from
+        torch.distributed."""
+        if fn is None:
+            self._xfn = EXCHANGE_FN()
+        else:
+            def _cb(user, buf, count, stream, _fn=fn):
+                try:
+                    return int(_fn(buf, count, stream or 0))
+                except Exception as e:  # a Python exception must not unwind through the C library
+                    self._xerr = e
+                    return 1
+            self._xfn = EXCHANGE_FN(_cb)  # kept alive with the context
+        self._check(lib().fms_set_exchange(self.h, self._xfn, None, int(rank), int(world)))
 
     def _check(self, rc: int, allow=()):
         if rc != 0 and rc not in allow:

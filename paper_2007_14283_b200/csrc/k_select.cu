@@ -256,23 +256,34 @@ __global__ void sel_write_kernel(Params p) {
     const float inv = p.inv[(size_t)f * p.n + i];
     const float* x = p.emb + ((size_t)f * p.n + i) * p.d;
     float* s = p.seeds + so * DP;
-    __half* sh = p.sop + ((size_t)f * p.S_pad + pos) * DP;
-    __half* ss = p.sops + ((size_t)f * p.S_pad + pos) * DP;
-    __half* sl = p.sopl + ((size_t)f * p.S_pad + pos) * DP;
+    // the operand row (and accumulators) of an active seed sit at its compacted position; with seed
+    // sharding only this rank's seeds (j % world == rank) are active here, at j / world
+    const bool own = pos % p.world == p.rank;
+    const int lp = pos / p.world;
+    __align__(16) __half sh[DP], ss[DP], sl[DP];
 #pragma unroll
     for (int k = 0; k < DP; ++k) {
       float v = k < p.d ? x[k] * inv : 0.f;
       s[k] = v;
       split_seed(v, sh[k], ss[k], sl[k]);
     }
-    double* g = p.gacc + ((size_t)f * p.S_pad + pos) * DP;
+    if (own) {
+      const size_t ro = (size_t)f * p.S_pad + lp;
 #pragma unroll
-    for (int k = 0; k < DP; ++k) g[k] = 0.0;
-    p.cacc[(size_t)f * p.S_pad + pos] = 0;
+      for (int k = 0; k < DP / 8; ++k) {
+        reinterpret_cast<uint4*>(p.sop + ro * DP)[k] = reinterpret_cast<const uint4*>(sh)[k];
+        reinterpret_cast<uint4*>(p.sops + ro * DP)[k] = reinterpret_cast<const uint4*>(ss)[k];
+        reinterpret_cast<uint4*>(p.sopl + ro * DP)[k] = reinterpret_cast<const uint4*>(sl)[k];
+      }
+      double* g = p.gacc + ro * DP;
+#pragma unroll
+      for (int k = 0; k < DP; ++k) g[k] = 0.0;
+      p.cacc[ro] = 0;
+      p.act[(size_t)f * p.S_cap + lp] = pos;
+    }
     p.sorig[so] = (int)i;
     p.sstat[so] = ST_ACTIVE;
     p.scnt[so] = 0;
-    p.act[so] = pos;
     p.flags[(size_t)f * p.n + i] |= PF_VISITED;
     ++pos;
   }
@@ -286,7 +297,8 @@ __global__ void sel_finish_kernel(Params p) {
   const int K = c.K_r;
   c.phase = PH_ITERATE;
   c.t = 0;
-  c.n_active = K;
+  const int mine = K > p.rank ? (K - 1 - p.rank) / p.world + 1 : 0;  // seeds this rank iterates
+  c.n_active = mine;
   c.n_conv = 0;
   const double g = p.kind == 2 ? 1.0 : p.gamma;
   double need = ceil(g * (double)K - 1e-9);
@@ -296,8 +308,8 @@ __global__ void sel_finish_kernel(Params p) {
   c.round_seed_iters[c.round] = 0;
   if (K == 0) { c.phase = PH_POST; }
   // rows [K, roundup(K, 128)) of the last seed tile are computed too; start them at zero
-  const int kpad = (K + kBM - 1) / kBM * kBM;
-  for (int r = K; r < kpad && r < p.S_pad; ++r) {
+  const int kpad = (mine + kBM - 1) / kBM * kBM;
+  for (int r = mine; r < kpad && r < p.S_pad; ++r) {
     double* g = p.gacc + ((size_t)f * p.S_pad + r) * p.DP;
     for (int k = 0; k < p.DP; ++k) g[k] = 0.0;
     p.cacc[(size_t)f * p.S_pad + r] = 0;

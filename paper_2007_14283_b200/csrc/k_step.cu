@@ -10,6 +10,8 @@
 // active (or max_iter), the remaining active seeds are discarded and the converged modes get one
 // count pass (their intensity |S_h(m)|, R10) before the merge phase; otherwise the active seeds
 // are compacted (ascending seed index) into the fp16 hi/lo operand rows.
+#include <algorithm>
+
 #include "fms_device.cuh"
 
 namespace fms {
@@ -125,7 +127,8 @@ __device__ int compact_seeds(const Params& p, int f, int K, uint8_t want, int* s
   int carry = 0;
   for (int j0 = 0; j0 < K; j0 += blockDim.x) {
     const int j = j0 + threadIdx.x;
-    const int a = (j < K && p.sstat[base + j] == want) ? 1 : 0;
+    // seed sharding: this rank iterates (and counts) only the seeds it owns
+    const int a = (j < K && p.sstat[base + j] == want && j % p.world == p.rank) ? 1 : 0;
     int tot;
     const int pos = carry + block_excl_scan(a, sm, &tot);
     if (a) {
@@ -164,13 +167,16 @@ __global__ void ctl_step_kernel(Params p) {
   }
   if (c.phase != PH_ITERATE) return;
   if (threadIdx.x == 0) {
-    const int A = c.n_active;
+    // decisions use the counts summed over the ranks (seed sharding); the compaction check uses
+    // this rank's own
+    int A = c.n_active, conv = c.step_conv, stall = c.step_stall;
+    if (p.world > 1) { A = p.xchg[f * 4 + 0]; conv = p.xchg[f * 4 + 1]; stall = p.xchg[f * 4 + 2]; }
     c.t += 1;
     c.seed_iters += A;
     c.round_seed_iters[c.round] += A;
-    c.n_conv += c.step_conv;
-    const int rem = A - c.step_conv - c.step_stall;
-    s_rem = rem;
+    c.n_conv += conv;
+    const int rem = A - conv - stall;
+    s_rem = c.n_active - c.step_conv - c.step_stall;
     s_end = (c.n_conv >= c.need) || rem <= 0 || c.t >= p.max_iter;
   }
   __syncthreads();
@@ -182,12 +188,13 @@ __global__ void ctl_step_kernel(Params p) {
     __syncthreads();
     const int r = c.round;
     const int nconv = c.n_conv;
-    if (nconv > 0) compact_seeds<DP>(p, f, K, ST_CONV, sm);  // rows for the intensity pass
+    // rows for the intensity pass (this rank's converged seeds; all of them without sharding)
+    const int nloc = nconv > 0 ? compact_seeds<DP>(p, f, K, ST_CONV, sm) : 0;
     if (threadIdx.x == 0) {
       c.round_iters[r] = c.t;
       c.round_conv[r] = nconv;
       c.round_disc[r] = K - nconv;
-      c.n_active = nconv;
+      c.n_active = nloc;
       if (r == 0 && nconv == 0) {
         c.status = 4;  // FMS_E_STALLED
         c.phase = PH_ERROR;
@@ -208,19 +215,95 @@ __global__ void ctl_step_kernel(Params p) {
   }
 }
 
+// ---------------- seed sharding: exchange buffers around the collectives ----------------
+// per step: this rank's (active, converged, stalled) counts -> xchg, summed over ranks before ctl_step
+__global__ void xchg_pack_kernel(Params p) {
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < p.B; f += gridDim.x * blockDim.x) {
+    const FrameCtl& c = p.ctl[f];
+    const bool it = c.phase == PH_ITERATE;
+    p.xchg[f * 4 + 0] = it ? c.n_active : 0;
+    p.xchg[f * 4 + 1] = it ? c.step_conv : 0;
+    p.xchg[f * 4 + 2] = it ? c.step_stall : 0;
+    p.xchg[f * 4 + 3] = 0;
+  }
+}
+// end of the round's iteration: largest K_r among frames about to merge -> counters[8]
+__global__ void xkmax_kernel(Params p) {
+  __shared__ int m;
+  if (threadIdx.x == 0) m = 0;
+  __syncthreads();
+  for (int f = threadIdx.x; f < p.B; f += blockDim.x)
+    if (p.ctl[f].phase == PH_POST) atomicMax(&m, p.ctl[f].K_r);
+  __syncthreads();
+  if (threadIdx.x == 0) p.counters[8] = m;
+}
+// owned seed rows (fp32 bits, status, intensity) into the round buffer, zeros elsewhere: summing
+// the buffer over ranks (int32) reproduces every owner's bits exactly, since one term is nonzero
+template <int DP>
+__global__ void xround_pack_kernel(Params p) {
+  const int f = blockIdx.y;
+  const FrameCtl& c = p.ctl[f];
+  const bool post = c.phase == PH_POST;
+  const int K = post ? c.K_r : 0;
+  const size_t base = (size_t)f * p.S_cap;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.xkmax; j += gridDim.x * blockDim.x) {
+    int* row = p.xbuf + ((size_t)f * p.xkmax + j) * (DP + 2);
+    const bool own = j < K && j % p.world == p.rank;
+#pragma unroll
+    for (int k = 0; k < DP; ++k) row[k] = own ? __float_as_int(p.seeds[(base + j) * DP + k]) : 0;
+    row[DP] = own ? (int)p.sstat[base + j] : 0;
+    row[DP + 1] = own ? p.scnt[base + j] : 0;
+  }
+}
+template <int DP>
+__global__ void xround_unpack_kernel(Params p) {
+  const int f = blockIdx.y;
+  const FrameCtl& c = p.ctl[f];
+  if (c.phase != PH_POST) return;
+  const int K = c.K_r;
+  const size_t base = (size_t)f * p.S_cap;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < K; j += gridDim.x * blockDim.x) {
+    const int* row = p.xbuf + ((size_t)f * p.xkmax + j) * (DP + 2);
+#pragma unroll
+    for (int k = 0; k < DP; ++k) p.seeds[(base + j) * DP + k] = __int_as_float(row[k]);
+    p.sstat[base + j] = (uint8_t)row[DP];
+    p.scnt[base + j] = row[DP + 1];
+  }
+}
+
+cudaError_t launch_xchg_pack(const Params& p, cudaStream_t st) {
+  xchg_pack_kernel<<<(p.B + 255) / 256, 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t launch_xkmax(const Params& p, cudaStream_t st) {
+  xkmax_kernel<<<1, 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t launch_xround(const Params& p, bool pack, cudaStream_t st) {
+  const dim3 g((unsigned)std::max(1, std::min(64, (p.xkmax + 255) / 256)), p.B);
+  if (p.DP == 16) {
+    if (pack) xround_pack_kernel<16><<<g, 256, 0, st>>>(p);
+    else xround_unpack_kernel<16><<<g, 256, 0, st>>>(p);
+  } else {
+    if (pack) xround_pack_kernel<32><<<g, 256, 0, st>>>(p);
+    else xround_unpack_kernel<32><<<g, 256, 0, st>>>(p);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_plan(const Params& p, cudaStream_t st) {
   plan_kernel<<<1, 1024, 0, st>>>(p);
   return cudaGetLastError();
 }
 
-cudaError_t launch_update_ctl(const Params& p, int num_sms, cudaStream_t st) {
-  if (p.DP == 16) {
-    update_kernel<16><<<num_sms * 4, kBM, 0, st>>>(p);
-    ctl_step_kernel<16><<<p.B, 256, 0, st>>>(p);
-  } else {
-    update_kernel<32><<<num_sms * 4, kBM, 0, st>>>(p);
-    ctl_step_kernel<32><<<p.B, 256, 0, st>>>(p);
-  }
+cudaError_t launch_update(const Params& p, int num_sms, cudaStream_t st) {
+  if (p.DP == 16) update_kernel<16><<<num_sms * 4, kBM, 0, st>>>(p);
+  else update_kernel<32><<<num_sms * 4, kBM, 0, st>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t launch_ctl(const Params& p, cudaStream_t st) {
+  if (p.DP == 16) ctl_step_kernel<16><<<p.B, 256, 0, st>>>(p);
+  else ctl_step_kernel<32><<<p.B, 256, 0, st>>>(p);
   return cudaGetLastError();
 }
 

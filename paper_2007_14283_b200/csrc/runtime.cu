@@ -29,8 +29,12 @@ cudaError_t launch_prep(const Params& p, cudaStream_t st);
 cudaError_t launch_select(const Params& p, int num_sms, cudaStream_t st);
 cudaError_t launch_plan(const Params& p, cudaStream_t st);
 cudaError_t launch_iter(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st);
-cudaError_t launch_update_ctl(const Params& p, int num_sms, cudaStream_t st);
 cudaError_t launch_post(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st);
+cudaError_t launch_update(const Params& p, int num_sms, cudaStream_t st);
+cudaError_t launch_ctl(const Params& p, cudaStream_t st);
+cudaError_t launch_xchg_pack(const Params& p, cudaStream_t st);
+cudaError_t launch_xkmax(const Params& p, cudaStream_t st);
+cudaError_t launch_xround(const Params& p, bool pack, cudaStream_t st);
 cudaError_t setup_assign_attrs();
 cudaError_t launch_output(const Params& p, float* centres_out, int cap, cudaStream_t st);
 cudaError_t setup_iter_attrs();
@@ -71,6 +75,10 @@ struct Ctx {
   size_t h_prof_cap = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  // seed sharding: the caller's in-place int32 sum over ranks (fms_set_exchange)
+  fms_exchange_fn xfn = nullptr;
+  void* xuser = nullptr;
+  int rank = 0, world = 1;
 };
 
 fms_status fail(Ctx* c, fms_status s, const std::string& m) {
@@ -159,6 +167,10 @@ size_t carve(Params& p, uint8_t* base) {
   p.sample = (unsigned long long*)take(B * (size_t)p.sample_cap * 8);
   p.blkcnt = (int*)take(B * (size_t)p.nblk * 4);
   p.ctl = (FrameCtl*)take(B * sizeof(FrameCtl));
+  if (p.world > 1) {  // seed-sharding exchange buffers
+    p.xchg = (int*)take((size_t)B * 4 * 4);
+    p.xbuf = (int*)take((size_t)B * p.S_cap * (p.DP + 2) * 4);
+  }
   return align_up(off, 1024);
 }
 
@@ -211,6 +223,8 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   p.H = pol->H;
   p.P = pol->P;
   p.rng_seed = pol->rng_seed;
+  p.rank = c->world > 1 ? c->rank : 0;
+  p.world = c->world > 1 ? c->world : 1;
   p.emb = emb;
   p.labels = labels;
   if (const char* v = getenv("FMS_ITER_VARIANT")) p.variant = atoi(v);  // timing experiments only
@@ -293,14 +307,33 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
         } else {
           CU(launch_iter(p.DP, tm, p, c->num_sms, st));
         }
-        CU(launch_update_ctl(p, c->num_sms, st));
+        CU(launch_update(p, c->num_sms, st));
+        if (p.world > 1) {  // seed sharding: per-frame step counts summed over the ranks
+          CU(launch_xchg_pack(p, st));
+          if (c->xfn(c->xuser, p.xchg, (int64_t)B * 4, st) != 0) return fail(c, FMS_E_NCCL, "step exchange failed");
+        }
+        CU(launch_ctl(p, st));
         ++steps;
-        kernels += 4;  // plan, iter, update, ctl_step
+        kernels += p.world > 1 ? 5 : 4;  // plan, iter, update, (exchange pack), ctl_step
       }
       CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
       CU(cudaStreamSynchronize(st));
       if (c->h_counters[5]) return fail(c, FMS_E_INTERNAL, "work-item capacity exceeded");
       if (c->h_counters[3] == 0) break;  // no frame still iterating
+    }
+    if (p.world > 1) {  // seed sharding: every rank gets every owner's converged seeds before the merge
+      CU(launch_xkmax(p, st));
+      CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      p.xkmax = c->h_counters[8];
+      if (p.xkmax > 0) {
+        CU(launch_xround(p, true, st));
+        if (c->xfn(c->xuser, p.xbuf, (int64_t)B * p.xkmax * (p.DP + 2), st) != 0)
+          return fail(c, FMS_E_NCCL, "round exchange failed");
+        CU(launch_xround(p, false, st));
+        kernels += 2;
+      }
+      kernels += 1;
     }
     CU(launch_post(p, tm, c->num_sms, st));
     kernels += 4;  // merge, assign (tensor cores), assign (CUDA cores, > 256 centres), osop
@@ -434,6 +467,19 @@ void fms_ctx_destroy(void* ctx) {
 const char* fms_last_error(const void* ctx) {
   const Ctx* c = static_cast<const Ctx*>(ctx);
   return c ? c->err.c_str() : "null context";
+}
+
+fms_status fms_set_exchange(void* ctx, fms_exchange_fn fn, void* user, int32_t rank, int32_t world) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c) return FMS_E_INVALID;
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !fn))
+    return fail(c, FMS_E_INVALID, "need 0 <= rank < world and an exchange function when world > 1");
+  c->xfn = fn;
+  c->xuser = user;
+  c->rank = rank;
+  c->world = world;
+  c->fresh_ws = true;  // the carve changes (exchange buffers)
+  return FMS_OK;
 }
 
 fms_status fms_set_option(void* ctx, const char* key, int64_t value) {

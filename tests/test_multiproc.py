@@ -2,6 +2,7 @@
 rank-0-only reference arm of bench.py (frames are independent, so the GPU path is replicas)."""
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -15,7 +16,7 @@ dist.init_process_group("gloo")
 import bench
 r = dist.get_rank()
 v = bench.reduce_max(10.0 + 5.0 * r, dist.get_world_size())
-print("RESULT", r, v, flush=True)
+sys.stdout.write(f"RESULT {r} {v}\n"); sys.stdout.flush()
 dist.destroy_process_group()
 """
 
@@ -32,8 +33,9 @@ def test_reduce_max_over_two_ranks(tmp_path):
     w.write_text(_WORKER % ROOT)
     out = _torchrun([str(w)])
     assert out.returncode == 0, out.stderr[-2000:]
-    res = [l.split() for l in out.stdout.splitlines() if l.startswith("RESULT")]
-    assert len(res) == 2 and all(float(x[2]) == 15.0 for x in res)
+    # the two ranks share stdout, so lines may interleave: match the records anywhere
+    res = re.findall(r"RESULT (\d+) ([0-9.]+)", out.stdout)
+    assert sorted(int(r) for r, _ in res) == [0, 1] and all(float(v) == 15.0 for _, v in res), out.stdout
 
 
 def test_reference_arm_rank0_only():
