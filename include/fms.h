@@ -112,7 +112,9 @@ const char* fms_version(void);
 typedef int (*fms_exchange_fn)(void* user, int32_t* buf, int64_t count, void* stream);
 fms_status fms_set_exchange(void* ctx, fms_exchange_fn fn, void* user, int32_t rank, int32_t world);
 
-/* Options: "profile_iter" (0/1): time every K2 launch with CUDA events for fms_run_stats.iter_ms. */
+/* Options: "profile_iter" (0/1): time every K2 launch with CUDA events for fms_run_stats.iter_ms.
+ *          "poll_steps" (1..64, default 4): lockstep steps launched between two host polls of the
+ *          device counters (a frame that finishes early idles at most poll_steps - 1 steps). */
 fms_status fms_set_option(void* ctx, const char* key, int64_t value);
 
 /* Cluster one frame.  emb: device, [n][d] fp32 row-major.  labels: device int32[n] in [0, K).

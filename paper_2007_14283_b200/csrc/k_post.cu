@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(1024) merge_kernel(Params p) {
   extern __shared__ uint8_t dsm[];
   __shared__ int sm[33];
   __shared__ unsigned s_supp;
+  __shared__ unsigned s_inb[32];  // in-batch conflicts: bit j of s_inb[i] = candidate j (< i) within rho
   __shared__ int s_kept, s_err;
 
   const int Kc = c.Kc;
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(1024) merge_kernel(Params p) {
   for (int base = 0; base < P; base += 32) {
     const int nb = min(32, P - base);
     if (threadIdx.x == 0) s_supp = 0;
+    if (threadIdx.x < 32) s_inb[threadIdx.x] = 0;
     for (int t = threadIdx.x; t < nb * DP; t += blockDim.x) {
       const int ci = t / DP, q = t - ci * DP;
       cand[t] = pool[(size_t)vals[base + ci] * DP + q];
@@ -124,12 +126,15 @@ __global__ void __launch_bounds__(1024) merge_kernel(Params p) {
       const float* kv = k < kKeptSm ? keptv + k * DP : cent + (size_t)k * DP;
       if (dotv<DP>(cand + ci * DP, kv) >= thr) atomicOr(&s_supp, 1u << ci);
     }
+    // all in-batch pairs (i, j < i) at once, one per thread, instead of a serial loop per lane
+    for (int idx = threadIdx.x; idx < 32 * 32; idx += blockDim.x) {
+      const int i = idx >> 5, j = idx & 31;
+      if (i < nb && j < i && dotv<DP>(cand + i * DP, cand + j * DP) >= thr) atomicOr(&s_inb[i], 1u << j);
+    }
     __syncthreads();
     if (warp == 0) {
       const float* a = cand + (lane < nb ? lane : 0) * DP;
-      unsigned inb = 0;
-      for (int j = 0; j < nb; ++j)
-        if (j < lane && dotv<DP>(a, cand + j * DP) >= thr) inb |= 1u << j;
+      const unsigned inb = lane < nb ? s_inb[lane] : 0u;
       const unsigned supp = s_supp;
       unsigned keep = 0;
       for (int i = 0; i < nb; ++i) {

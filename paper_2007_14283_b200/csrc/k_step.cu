@@ -297,8 +297,8 @@ cudaError_t launch_plan(const Params& p, cudaStream_t st) {
 }
 
 cudaError_t launch_update(const Params& p, int num_sms, cudaStream_t st) {
-  if (p.DP == 16) update_kernel<16><<<num_sms * 4, kBM, 0, st>>>(p);
-  else update_kernel<32><<<num_sms * 4, kBM, 0, st>>>(p);
+  if (p.DP == 16) update_kernel<16><<<num_sms, kBM, 0, st>>>(p);  // grid-stride over the step's tiles
+  else update_kernel<32><<<num_sms, kBM, 0, st>>>(p);
   return cudaGetLastError();
 }
 cudaError_t launch_ctl(const Params& p, cudaStream_t st) {

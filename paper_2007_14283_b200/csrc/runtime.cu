@@ -45,7 +45,7 @@ using namespace fms;
 
 namespace {
 
-constexpr int kPoll = 4;            // lockstep steps launched between host polls
+constexpr int kPoll = 4;            // default lockstep steps launched between host polls
 constexpr int kMaxPcap = 8192;      // merge pool capacity (SMEM bitonic sort)
 constexpr int kCounters = 64;
 
@@ -79,6 +79,7 @@ struct Ctx {
   fms_exchange_fn xfn = nullptr;
   void* xuser = nullptr;
   int rank = 0, world = 1;
+  int poll = kPoll;  // lockstep steps between host polls ("poll_steps")
 };
 
 fms_status fail(Ctx* c, fms_status s, const std::string& m) {
@@ -275,8 +276,8 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   for (int round = 0; round < pol->max_rounds + 1; ++round) {
     CU(launch_select(p, c->num_sms, st));
     kernels += 7;
-    for (int s = 0; s < max_iters + kPoll; s += kPoll) {
-      for (int k = 0; k < kPoll; ++k) {
+    for (int s = 0; s < max_iters + c->poll; s += c->poll) {
+      for (int k = 0; k < c->poll; ++k) {
         CU(launch_plan(p, st));
         if (c->profile) {
           const size_t slot = launches;
@@ -487,6 +488,11 @@ fms_status fms_set_option(void* ctx, const char* key, int64_t value) {
   if (!c || !key) return FMS_E_INVALID;
   if (!strcmp(key, "profile_iter")) {
     c->profile = value != 0;
+    return FMS_OK;
+  }
+  if (!strcmp(key, "poll_steps")) {  // a frame that finishes idles at most poll_steps - 1 steps
+    if (value < 1 || value > 64) return fail(c, FMS_E_INVALID, "poll_steps must be in 1..64");
+    c->poll = (int)value;
     return FMS_OK;
   }
   return fail(c, FMS_E_INVALID, std::string("unknown option ") + key);
