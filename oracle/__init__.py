@@ -69,6 +69,8 @@ def lib():
         L.fmso_p_success.argtypes = [C.c_int64, C.c_int64, C.c_double]
         L.fmso_n_min.restype = C.c_int64
         L.fmso_n_min.argtypes = [C.c_double, C.c_int64, C.c_double]
+        L.fmso_session_next.restype = C.c_int64
+        L.fmso_session_next.argtypes = [C.c_int64, C.c_double, C.c_double]
         L.fmso_need.restype = C.c_int32
         L.fmso_need.argtypes = [C.c_double, C.c_int64]
         L.fmso_normalize.restype = C.c_int
@@ -205,6 +207,32 @@ def p_success(N: int, I: int, r: float) -> float:
 
 def n_min(P: float, I: int, r: float) -> int:
     return lib().fmso_n_min(P, I, r)
+
+
+def session_next(total: int, nmin: float, H: float) -> int:
+    """O8: seed count carried to the next frame (R12, R18); nmin < 0 = infinite."""
+    return lib().fmso_session_next(int(total), float(nmin), float(H))
+
+
+def session(frames, h: float = 0.1, max_iter: int = 300, tol: float | None = None, pol: Policy | None = None,
+            centres_cap: int = 65536):
+    """NEXT-1: cluster a frame sequence, carrying the OSOP seed count N across frames (O8): frame
+    t's round 0 uses N_t seeds; N_{t+1} = session_next(seeds used by frame t, its last N_min, H).
+    Returns (results, N sequence)."""
+    pol = pol if pol is not None else policy()
+    N = int(pol.n_seeds)
+    out, Ns = [], []
+    for emb in frames:
+        p = policy(pol.kind, N, pol.gamma, pol.L, pol.H, pol.P, pol.has_background, pol.min_instance_px,
+                   pol.saturation_stop, pol.max_rounds, pol.rng_seed)
+        r = cluster(emb, h=h, max_iter=max_iter, tol=tol, pol=p, centres_cap=centres_cap)
+        out.append(r)
+        Ns.append(N)
+        if r.status != 0:
+            break
+        nm = r.trace["round_nmin"][-1] if r.trace["rounds"] > 0 else -1.0
+        N = max(1, session_next(r.trace["seeds_total"], nm, pol.H))
+    return out, Ns
 
 
 def key(rng_seed: int, round_: int, i: int) -> int:

@@ -72,6 +72,21 @@ int32_t fmso_need(double gamma, int64_t K) {
   return (int32_t)v;
 }
 
+/* O8 (NEXT-1): the seed count carried to the next frame of a sequence.  P:318: "The N will be
+ * doubled for the next iteration [within a frame, R12] ... if N is too large compared to N_min, N
+ * is reduced as N - N_min" with "too large" = N > H N_min (Eq. 21's upper bound, H = 8 P:318);
+ * R18: floor at N_min.  The frame's N is the total number of seeds it used; N_min is the last
+ * estimate (Eq. 19) of the frame. */
+int64_t fmso_session_next(int64_t total, double nmin, double H) {
+  if (!(nmin > 0.0)) return total; /* N_min infinite: nothing to reduce against */
+  if ((double)total > H * nmin) {
+    const int64_t m = (int64_t)nmin;
+    const int64_t v = total - m;
+    return v > m ? v : m;
+  }
+  return total;
+}
+
 /* ---------------------------------------------------------------------------------------------
  * Eq. 1 / Eq. 9: cosine distance is 1 - x.y/(|x||y|), so every embedding is
  * divided by its Euclidean norm once.  A zero or non-finite norm has no direction -> error.

@@ -54,6 +54,10 @@ uint64_t fmso_key(uint64_t rng_seed, int32_t round, int64_t i);
 double fmso_p_success(int64_t N, int64_t I, double r);      /* Eq. 14 */
 int64_t fmso_n_min(double P, int64_t I, double r);           /* Eq. 19; INT64_MAX if I == 0 */
 int32_t fmso_need(double gamma, int64_t K);                  /* ceil(gamma*K) (R8) */
+/* O8 / NEXT-1, the frame-to-frame seed count ("N is reduced as N - N_min", R12, R18):
+ * N_next = total seeds of the frame; if N_next > H * N_min then N_next = max(N_next - N_min, N_min).
+ * nmin < 0 means N_min = infinity (no instance observed): N_next = total. */
+int64_t fmso_session_next(int64_t total, double nmin, double H);
 
 /* ---- vector pieces ---- */
 int fmso_normalize(const float* emb, int64_t n, int32_t d, double* xhat);         /* Eq. 1 / 9 */

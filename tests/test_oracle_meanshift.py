@@ -297,3 +297,17 @@ def test_determinism_across_thread_counts(tmp_path):
         subprocess.check_call([sys.executable, "-c", code, p], env=env)
         outs.append(np.load(p))
     assert outs[0].tobytes() == outs[1].tobytes()
+
+
+def test_session_carries_seed_count_between_frames():
+    """NEXT-1 / O8: frame t+1's round 0 uses the seed count session_next() derived from frame t."""
+    import synth
+    from synth.frames import min_instance_px
+    frames = [synth.make_frame("S1", s).emb for s in range(3)]
+    pol = oracle.policy(min_instance_px=min_instance_px(frames[0].shape[0]), saturation_stop=1, n_seeds=32)
+    res, Ns = oracle.session(frames, pol=pol)
+    assert Ns[0] == 32 and all(r.status == 0 for r in res)
+    for t in range(1, len(res)):
+        prev = res[t - 1].trace
+        assert Ns[t] == oracle.session_next(prev["seeds_total"], prev["round_nmin"][-1], pol.H)
+        assert res[t].trace["round_K"][0] == min(Ns[t], frames[t].shape[0])

@@ -124,3 +124,22 @@ def test_select_uniform_inclusion():
     p = K / n
     sd = math.sqrt(salts * p * (1 - p))
     assert np.all(np.abs(cnt - salts * p) <= 4.5 * sd)
+
+
+@pytest.mark.parametrize("row", range(5))
+def test_session_next_worked_values(golden, row):
+    """O8 / NEXT-1 frame-to-frame seed count against SPEC's worked controller examples."""
+    e = golden["session_next"][row]
+    assert oracle.session_next(e["total"], e["nmin"], e["H"]) == e["N"]
+
+
+def test_session_reaches_dead_band_on_a_stationary_sequence():
+    """SPEC S:296 controller safety: with stationary (I, r) repeated updates stop changing once N is
+    inside the dead band (N <= H N_min), and never go below N_min."""
+    nmin, H = 100.0, 8.0
+    N = 5000
+    seen = [N]
+    for _ in range(100):
+        N = oracle.session_next(N, nmin, H)
+        seen.append(N)
+    assert seen[-1] == seen[-2] <= H * nmin and min(seen) >= nmin
