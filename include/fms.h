@@ -95,6 +95,21 @@ void fms_ctx_destroy(void* ctx);
 const char* fms_last_error(const void* ctx);
 const char* fms_version(void);
 
+/* Frame sequences (NEXT-1; the seed count N is carried from frame to
+ * frame).  A session clusters one frame per fms_session_step with round 0 using the session's N
+ * (initially policy->n_seeds); afterwards N = the frame's total seeds, reduced to
+ * max(N - N_min, N_min) when N > H * N_min, N_min being the frame's last Eq. 19 estimate.
+ * fms_session_step takes the arguments of fms_cluster (same ownership, errors and blocking) and
+ * updates N only when the frame succeeded (FMS_OK or FMS_E_CAPACITY).  policy must be OSOP
+ * (FMS_E_INVALID otherwise); the policy is copied.  fms_session_seeds returns the N the next
+ * frame will start with (-1 for a NULL session).  The session borrows ctx (destroy it first). */
+fms_status fms_session_create(void* ctx, const fms_seed_policy* policy, void** session_out);
+fms_status fms_session_step(void* session, const float* emb, int64_t n, int32_t d, double bandwidth,
+                            int32_t max_iters, double tol, int32_t* labels, float* centres, int32_t centres_cap,
+                            int32_t* K_out, fms_frame_stats* frame_stats, fms_run_stats* run_stats, void* stream);
+int64_t fms_session_seeds(const void* session);
+void fms_session_destroy(void* session);
+
 /* Seed sharding (the seeds of a round are independent mean-shift trajectories,
  * Alg. 2 l.4-9, so a round's seeds can be split over GPUs that each hold the
  * whole frame).  With world > 1, rank r iterates only the round seeds j with j % world == r; the

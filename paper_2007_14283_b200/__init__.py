@@ -15,7 +15,8 @@ MAX_ROUNDS = 16
 STATUS = {0: "OK", 2: "INVALID", 3: "ZERO_NORM", 4: "STALLED", 5: "CAPACITY", 6: "CUDA", 7: "NCCL", 8: "OOM",
           9: "INTERNAL"}
 EXPORTS = ["fms_default_policy", "fms_ctx_create", "fms_ctx_destroy", "fms_last_error", "fms_version",
-           "fms_set_option", "fms_set_exchange", "fms_cluster", "fms_cluster_batch", "fms_cluster_batch_host"]
+           "fms_set_option", "fms_set_exchange", "fms_cluster", "fms_cluster_batch", "fms_cluster_batch_host",
+           "fms_session_create", "fms_session_step", "fms_session_seeds", "fms_session_destroy"]
 
 # int (*)(void* user, int32_t* buf, int64_t count, void* stream): in-place int32 sum over ranks
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
@@ -81,6 +82,14 @@ def lib() -> C.CDLL:
         L.fms_ctx_destroy.restype = None
         L.fms_set_option.argtypes = [vp, C.c_char_p, i64]
         L.fms_set_exchange.argtypes = [vp, EXCHANGE_FN, vp, i32, i32]
+        L.fms_session_create.argtypes = [vp, C.POINTER(Policy), C.POINTER(vp)]
+        L.fms_session_create.restype = C.c_int
+        L.fms_session_step.argtypes = [vp, vp, i64, i32] + [f64, i32, f64, vp, vp, i32, vp, vp, C.POINTER(RunStats), vp]
+        L.fms_session_step.restype = C.c_int
+        L.fms_session_seeds.argtypes = [vp]
+        L.fms_session_seeds.restype = i64
+        L.fms_session_destroy.argtypes = [vp]
+        L.fms_session_destroy.restype = None
         common = [f64, i32, f64, C.POINTER(Policy), vp, vp, i32, vp, vp, C.POINTER(RunStats), vp]
         L.fms_cluster.argtypes = [vp, vp, i64, i32] + common
         L.fms_cluster_batch.argtypes = [vp, vp, i32, i64, i32] + common
@@ -202,6 +211,55 @@ class Context:
                                           C.byref(rs), C.c_void_p(stream))
         self._check(rc, allow)
         return rc, list(K), rs.as_dict()
+
+
+class Session:
+    """NEXT-1 frame sequence (include/fms.h fms_session_*): the OSOP seed count N carries from one
+    frame to the next."""
+
+    def __init__(self, ctx: Context, policy: Policy | None = None):
+        self.ctx = ctx
+        policy = policy if policy is not None else default_policy()
+        h = C.c_void_p()
+        ctx._check(lib().fms_session_create(ctx.h, C.byref(policy), C.byref(h)))
+        self.h = h
+
+    @property
+    def seeds(self) -> int:
+        """N for round 0 of the next frame."""
+        return int(lib().fms_session_seeds(self.h))
+
+    def step(self, emb, h: float = 0.1, max_iters: int = 300, tol: float | None = None, centres_cap: int = 4096,
+             allow=()):
+        """emb: CUDA float32 [n, d].  Returns (labels [n], centres [cap, d], K, frame stats)."""
+        import torch
+        if not (emb.is_cuda and emb.dtype == torch.float32 and emb.dim() == 2):
+            raise TypeError("emb must be a CUDA float32 tensor [n, d]")
+        emb = emb.contiguous()
+        n, d = emb.shape
+        tol = h / 1000.0 if tol is None else tol
+        labels = torch.empty((n,), dtype=torch.int32, device=emb.device)
+        centres = torch.zeros((max(centres_cap, 1), d), dtype=torch.float32, device=emb.device)
+        K = C.c_int32()
+        fs = FrameStats()
+        rs = RunStats()
+        stream = torch.cuda.current_stream(emb.device).cuda_stream
+        rc = lib().fms_session_step(self.h, C.c_void_p(emb.data_ptr()), n, d, h, max_iters, tol,
+                                    C.c_void_p(labels.data_ptr()), C.c_void_p(centres.data_ptr()), centres_cap,
+                                    C.byref(K), C.byref(fs), C.byref(rs), C.c_void_p(stream))
+        self.ctx._check(rc, allow)
+        return labels, centres, K.value, fs.as_dict()
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().fms_session_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 _ctxs: dict[int, Context] = {}

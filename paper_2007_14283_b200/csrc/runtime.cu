@@ -514,6 +514,55 @@ fms_status fms_cluster(void* ctx, const float* emb, int64_t n, int32_t d, double
                            K_out, frame_stats, run_stats, stream);
 }
 
+// ---- NEXT-1: frame sequences with the seed count carried across frames (O8) ----
+struct Session {
+  Ctx* c;
+  fms_seed_policy pol;
+  int64_t N;  // seeds for round 0 of the next frame
+};
+
+// P:318 "if N is too large compared to N_min, N is reduced as N - N_min": N_next = the frame's
+// total seeds; reduced by N_min when above H * N_min, never below N_min (R18); N_min = the frame's
+// last Eq. 19 estimate (-1 = infinite: no reduction)
+static int64_t session_next(int64_t total, double nmin, double H) {
+  if (!(nmin > 0.0) || !((double)total > H * nmin)) return total;
+  const int64_t m = (int64_t)nmin;
+  return std::max<int64_t>(total - m, m);
+}
+
+fms_status fms_session_create(void* ctx, const fms_seed_policy* policy, void** session_out) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c || !policy || !session_out) return FMS_E_INVALID;
+  if (policy->kind != FMS_SEEDS_OSOP) return fail(c, FMS_E_INVALID, "sessions carry the OSOP seed count");
+  if (policy->n_seeds < 1) return fail(c, FMS_E_INVALID, "n_seeds must be >= 1");
+  *session_out = new Session{c, *policy, policy->n_seeds};
+  return FMS_OK;
+}
+
+int64_t fms_session_seeds(const void* session) {
+  return session ? static_cast<const Session*>(session)->N : -1;
+}
+
+void fms_session_destroy(void* session) { delete static_cast<Session*>(session); }
+
+fms_status fms_session_step(void* session, const float* emb, int64_t n, int32_t d, double bandwidth,
+                            int32_t max_iters, double tol, int32_t* labels, float* centres, int32_t centres_cap,
+                            int32_t* K_out, fms_frame_stats* frame_stats, fms_run_stats* run_stats, void* stream) {
+  Session* s = static_cast<Session*>(session);
+  if (!s) return FMS_E_INVALID;
+  fms_seed_policy pol = s->pol;
+  pol.n_seeds = (int32_t)std::min<int64_t>(s->N, INT32_MAX);
+  fms_frame_stats fs{};
+  fms_status r = fms_cluster(s->c, emb, n, d, bandwidth, max_iters, tol, &pol, labels, centres, centres_cap, K_out,
+                             &fs, run_stats, stream);
+  if (frame_stats) *frame_stats = fs;
+  if (r == FMS_OK || r == FMS_E_CAPACITY) {
+    const double nmin = fs.rounds > 0 ? fs.round_nmin[fs.rounds - 1] : -1.0;
+    s->N = std::max<int64_t>(1, session_next(fs.seeds_total, nmin, s->pol.H));
+  }
+  return r;
+}
+
 fms_status fms_cluster_batch_host(void* ctx, const float* emb_host, int32_t B, int64_t n, int32_t d,
                                   double bandwidth, int32_t max_iters, double tol,
                                   const fms_seed_policy* policy, int32_t* labels_host, float* centres_host,

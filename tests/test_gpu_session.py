@@ -1,0 +1,29 @@
+"""NEXT-1: frame sequences with the OSOP seed count carried across frames (O8) -- the CUDA
+path's fms_session_* against the oracle's session on identical seeded frames."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth.frames import min_instance_px
+from tests.parity_util import bijection, match_centres
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("cfg,n_seeds", [("S1sep", 32), ("C2sep", 128)])
+def test_session_matches_oracle_session(cfg, n_seeds):
+    import torch
+    import paper_2007_14283_b200 as fms
+    frames = [synth.make_frame(cfg, s).emb for s in range(4)]
+    mp = min_instance_px(frames[0].shape[0])
+    ro, Ns = oracle.session(frames, pol=oracle.policy(n_seeds=n_seeds, min_instance_px=mp, saturation_stop=1))
+    sess = fms.Session(fms.context(0), fms.default_policy(n_seeds=n_seeds, min_instance_px=mp, saturation_stop=1))
+    for t, emb in enumerate(frames):
+        assert sess.seeds == Ns[t]
+        labels, centres, K, fs = sess.step(torch.from_numpy(emb).cuda(), centres_cap=1024)
+        assert K == ro[t].K and fs["round_K"] == ro[t].trace["round_K"]
+        assert bijection(labels.cpu().numpy(), ro[t].labels)
+        _, _, dist = match_centres(centres[:K].cpu().numpy(), ro[t].centres)
+        assert dist.max() <= 1e-4
+    assert sess.seeds == oracle.session_next(ro[-1].trace["seeds_total"], ro[-1].trace["round_nmin"][-1], 8.0)
