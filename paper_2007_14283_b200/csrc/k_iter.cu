@@ -361,13 +361,14 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         const uint32_t pb = ctile % Cfg::NP;
         tc_fence_after();
         uint32_t v[kColsPerWarp];
+        if (K2_OFF(p, 128) && lane == 0) mbar_arrive(&c_empty[grp]);  // timing experiment: release early
         if (!K2_OFF(p, 16)) {
           tmem_ld64(cbase, v);  // one instruction: the scheduler cannot interleave math between pieces
           tmem_ld_wait();
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&c_empty[grp]);  // MMA1 may overwrite C[grp]
+        if (!K2_OFF(p, 128) && lane == 0) mbar_arrive(&c_empty[grp]);  // MMA1 may overwrite C[grp]
         tlog(p, lrole, ctile, 2);
         // P[pb] is free once the weighted sum of the tile that used it last has completed: probe
         // now, use the answer after the flat kernel

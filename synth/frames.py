@@ -141,3 +141,15 @@ def frame_pool(config: str, count: int, base_seed: int = 0) -> list[Frame]:
 def min_instance_px(n: int) -> int:
     """SURVEY R22 proposal: 200 px at 512x512, scaled with the pixel count."""
     return max(1, int(round(200.0 * n / 262144.0)))
+
+
+def make_blobs(n: int, seed: int, D: int = 18, k: int = 10, std: float = 0.01):
+    """PAPER.md P:336 (Table 1 design): n points in D = 18 dimensions from k = 10 clusters
+    (`blobs`), Gaussian noise of standard deviation 0.01, cluster directions orthogonal or opposite
+    (signed basis vectors).  Equal-size clusters in random order.  Returns (emb float32 [n, D],
+    truth int32 [n])."""
+    rng = np.random.default_rng(np.random.SeedSequence([int(seed), 7777, int(n)]))
+    dirs = _directions(rng, k, D)
+    truth = rng.permutation(np.arange(n) % k).astype(np.int32)
+    x = dirs[truth] + std * rng.standard_normal((n, D))
+    return np.ascontiguousarray(x, dtype=np.float32), truth

@@ -149,6 +149,14 @@ def test_more_than_128_modes_exact():
     assert ro.K > 128 and max(ro.trace["round_Kc"]) > 128
 
 
+@pytest.mark.parametrize("n,kind", [(1000, 2), (2000, 2), (5000, 1)])
+def test_table1_blobs_exact(n, kind):
+    """NEXT-3: the paper's Table 1 simulation data (18-D blobs, 10 orthogonal/opposite
+    clusters, noise 0.01) under Alg. 1 (kind 2, every point a seed) and OSOP: exact vs the oracle."""
+    emb, _ = synth.make_blobs(n, seed=1)
+    check_exact(emb, kind=kind, n_seeds=128, has_background=0)
+
+
 # ---------------------------------------------------------------------------------------------
 # batching, determinism, host entry
 # ---------------------------------------------------------------------------------------------

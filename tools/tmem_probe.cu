@@ -24,6 +24,9 @@ __device__ __forceinline__ void ld_32x32b_x32_pack(uint32_t taddr, uint32_t (&v)
       : "r"(taddr));
 }
 
+__device__ __forceinline__ void ld_x64(uint32_t taddr, uint32_t (&v)[64]) { tmem_ld64(taddr, v); }
+__device__ __forceinline__ void ld_x128(uint32_t taddr, uint32_t (&v)[128]) { tmem_ld128(taddr, v); }
+
 template <int SHAPE>
 __global__ void probe(int reps, unsigned long long* out, unsigned* sink) {
   __shared__ uint32_t holder;
@@ -52,12 +55,24 @@ __global__ void probe(int reps, unsigned long long* out, unsigned* sink) {
       tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 32; ++i) acc ^= v[i];
-    } else {
+    } else if (SHAPE == 2) {
       uint32_t v[16];
       ld_32x32b_x32_pack(tmem + lane_base + col, v);
       tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc ^= v[i];
+    } else if (SHAPE == 3) {
+      uint32_t v[64];
+      ld_x64(tmem + lane_base + ((col * 2) & 511), v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 64; ++i) acc ^= v[i];
+    } else {
+      uint32_t v[128];
+      ld_x128(tmem + lane_base + ((col * 4) & 511), v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 128; ++i) acc ^= v[i];
     }
   }
   __syncthreads();
@@ -77,12 +92,15 @@ int main() {
   cudaMalloc(&sink, 4);
   unsigned long long h[148];
   const int reps = 256;
-  for (int shape = 0; shape < 3; ++shape) {
+  for (int shape = 0; shape < 5; ++shape) {
+    if (shape == 1) continue;  // 16x256b needs a different lane mapping (not used)
     for (int warps : {4, 8, 16}) {
       for (int it = 0; it < 2; ++it) {
         if (shape == 0) probe<0><<<148, warps * 32>>>(reps, d, sink);
         else if (shape == 1) probe<1><<<148, warps * 32>>>(reps, d, sink);
-        else probe<2><<<148, warps * 32>>>(reps, d, sink);
+        else if (shape == 2) probe<2><<<148, warps * 32>>>(reps, d, sink);
+        else if (shape == 3) probe<3><<<148, warps * 32>>>(reps, d, sink);
+        else probe<4><<<148, warps * 32>>>(reps, d, sink);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
       }
@@ -91,8 +109,9 @@ int main() {
       for (int i = 0; i < 148; ++i) avg += h[i];
       avg /= 148;
       // bytes read from TMEM per CTA: warps * reps * 32 lanes * 32 columns * 4 B (pack::16b: same cells)
-      const double bytes = (double)warps * reps * 32 * 32 * 4;
-      const char* nm[] = {"32x32b.x32", "16x256b.x8", "32x32b.x32.pack16"};
+      const double mult = shape == 3 ? 2.0 : shape == 4 ? 4.0 : 1.0;
+      const double bytes = (double)warps * reps * 32 * 32 * 4 * mult;
+      const char* nm[] = {"32x32b.x32", "16x256b.x8", "32x32b.x32.pack16", "32x32b.x64", "32x32b.x128"};
       printf("%-18s warps=%2d : %8.0f cycles, %6.1f TMEM bytes/cycle/SM\n", nm[shape], warps, avg, bytes / avg);
     }
   }
