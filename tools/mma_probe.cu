@@ -255,6 +255,50 @@ __global__ void alu_mix(int mode, int iters, unsigned long long* out, uint32_t* 
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// do tcgen05.ld traffic and MMA execution contend?  warp 0 issues `reps` SS N=128 MMAs (into columns
+// 256..383) while warps 4..11 (2 per SM sub-partition) stream 32x32b.x64 loads from columns 0..255
+__global__ void tmem_mma(int reps, int loads, unsigned long long* out, unsigned* sink) {
+  __shared__ __align__(1024) uint8_t sm[40 * 1024];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t holder;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 40 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3C003C00u;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  if (warp == 0) tmem_alloc(&holder, 512);
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = holder;
+  unsigned long long t0 = clock64();
+  if (warp == 0) {
+    if (reps > 0) {
+      const uint64_t ad = umma_desc(smem_u32(sm), 16, 256, 6), bd = umma_desc(smem_u32(sm + 8192), 16, 256, 6);
+      for (int r = 0; r < reps; ++r) mma_ss_el(tmem + 256 + (r & 1) * 128, ad, bd, idesc_f16(128, 128, 0, 0), r >= 2);
+      commit_el(&bar);
+      __syncwarp();
+      mbar_wait(&bar, 0);
+    }
+  } else if (warp >= 4 && warp < 12 && loads > 0) {
+    const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
+    uint32_t acc = 0;
+    for (int r = 0; r < loads; ++r) {
+      uint32_t v[64];
+      tmem_ld64(tmem + lb + ((warp >> 2) & 1) * 64 + (r & 1) * 128, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 64; ++i) acc ^= v[i];
+    }
+    if (acc == 0x1234567u) sink[0] = acc;
+  }
+  unsigned long long t1 = clock64();
+  if (lane == 0 && (warp == 0 || warp == 4)) out[blockIdx.x * 2 + (warp == 4)] = t1 - t0;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 8 * 148);
@@ -332,6 +376,24 @@ int main() {
       for (int i = 0; i < 148; ++i) { w4 += h3[2 * i]; w5 += h3[2 * i + 1]; }
       printf("alu_mix: warp0 %-14s -> epilogue-like loop warp4 (same SMSP) %.0f cyc, warp5 (other SMSP) %.0f cyc (%.2f cyc per pair)\n",
              nm[mode], w4 / 148, w5 / 148, w5 / 148 / (300.0 * 32));
+    }
+  }
+  {
+    unsigned long long* d4;
+    unsigned* sink4;
+    cudaMalloc(&d4, 16 * 148);
+    cudaMalloc(&sink4, 4);
+    unsigned long long h4[296];
+    const int cfg[][2] = {{200, 0}, {0, 400}, {200, 400}};
+    for (auto& c : cfg) {
+      for (int it = 0; it < 2; ++it) tmem_mma<<<148, 384>>>(c[0], c[1], d4, sink4);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+      cudaMemcpy(h4, d4, 16 * 148, cudaMemcpyDeviceToHost);
+      double a = 0, b = 0;
+      for (int i = 0; i < 148; ++i) { a += h4[2 * i]; b += h4[2 * i + 1]; }
+      printf("tmem_mma: %3d SS N=128 MMAs (%.0f cyc) + 8 warps x %3d LDTM.x64 (%.0f cyc)\n", c[0], c[0] ? a / 148 : 0.0,
+             c[1], c[1] ? b / 148 : 0.0);
     }
   }
   unsigned long long* d2;
