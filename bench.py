@@ -42,6 +42,8 @@ def parse():
                     help="replicas: every rank clusters its own frames (weak scaling); seeds: every rank "
                          "clusters the same frames and iterates 1/N of each round's seeds (strong scaling, "
                          "SURVEY 8(e)2; exchange through torch.distributed)")
+    ap.add_argument("--no-seed-shard", action="store_true",
+                    help="with N > 1 replicas: skip the extra seed-sharded C4 measurement")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend of the fms arm (gloo: several ranks may share one GPU)")
     return ap.parse_args()
@@ -162,6 +164,48 @@ def cpu_baseline(frames, budget_s=20.0):
                       f"fp64 C oracle with OpenMP, {dt:.1f} s"}
 
 
+def seed_sharded_c4(world, rank, local, B=2, warmup=1, steps=3):
+    """SURVEY 8(e)2 / BASELINE configs[3]: the same C4 frames (1024x1024, 32-D, ~200 cells) on every
+    rank, each rank iterating 1/world of every round's seeds (strong scaling), next to the same
+    frames clustered by one rank alone.  Device time, max over ranks."""
+    import numpy as np
+    import torch
+
+    import paper_2007_14283_b200 as fms
+    import synth
+    from paper_2007_14283_b200.dist import enable_seed_sharding
+    dev = torch.device("cuda", local)
+    frames = [synth.make_frame("C4", 30000 + i) for i in range(B)]
+    n, d = frames[0].n, frames[0].D
+    x = torch.from_numpy(np.stack([f.emb for f in frames])).to(dev)
+    labels = torch.empty((B, n), dtype=torch.int32, device=dev)
+    cent = torch.empty((B, CAP, d), dtype=torch.float32, device=dev)
+    pol = fms.default_policy(**policy_kwargs(n))
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(ctx):
+        Ks = None
+        for _ in range(warmup):
+            ctx.cluster_batch_ptr(x.data_ptr(), B, n, d, labels.data_ptr(), cent.data_ptr(), CAP, H, MAX_ITERS, None,
+                                  pol, stream.cuda_stream)
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            _, Ks, _, _ = ctx.cluster_batch_ptr(x.data_ptr(), B, n, d, labels.data_ptr(), cent.data_ptr(), CAP, H,
+                                                MAX_ITERS, None, pol, stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return reduce_max(e0.elapsed_time(e1), world, dev), Ks
+
+    single_ms, K1 = timed(fms.Context(local))
+    sharded_ms, KN = timed(enable_seed_sharding(fms.Context(local)))
+    return {"config": "C4: 1024x1024, 32-D, 200 cells, full OSOP", "frames_per_step": B, "n_gpus": world,
+            "value": steps * B / (sharded_ms / 1e3), "unit": "frames/s", "scaling": "strong",
+            "one_rank_value": steps * B / (single_ms / 1e3), "K_equal_to_one_rank": K1 == KN}
+
+
 def run_reference(args, world, rank):
     if rank != 0:  # the reference arm runs on rank 0 only; other ranks exit 0 without work
         return
@@ -266,6 +310,13 @@ def main():
         e2e = {"value": ksteps * B * (1 if sharded else world) / (ems / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": B * n * d * 4, "d2h_bytes_per_step": B * n * 4 + B * CAP * d * 4}
 
+    seed_sh = None
+    if world > 1 and not sharded and not args.no_seed_shard:
+        try:
+            seed_sh = seed_sharded_c4(world, rank, local)
+        except Exception as e:  # reported, not fatal: the replicas line above is the headline
+            seed_sh = {"error": f"{type(e).__name__}: {e}"[:300]}
+
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -304,6 +355,8 @@ def main():
         "e2e": e2e,
         "cpu_baseline": cb,
     }
+    if seed_sh is not None:
+        line["seed_sharded"] = seed_sh
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
