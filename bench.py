@@ -333,6 +333,16 @@ def main():
             "iter_share_of_step": totals["iter_ms"] / ms if ms > 0 else None}
     # frame-level roofline: algorithmic iteration FLOPs of the whole job at the tensor peak
     frame_roof_ms = flops / (peak * 1e12) * 1e3
+    # north_star / SURVEY 8(d): the job's roofline is the slowest of three limits -- contraction FLOPs
+    # at the tensor peak, kernel exponentials at the SFU peak (0: the flat kernel has none, Eq. 3/11),
+    # and embedding bytes at HBM bandwidth (read the fp32 input once, write labels)
+    job_frames = totals["frames"]
+    hbm_bytes = job_frames * (n * d * 4 + n * 4)
+    hbm_ms = hbm_bytes / (peaks["hbm_gbs"] * 1e9) * 1e3
+    roof_terms = {"tensor_ms": frame_roof_ms, "sfu_ms": 0.0, "hbm_ms": hbm_ms,
+                  "bound": "tensor" if frame_roof_ms >= hbm_ms else "hbm",
+                  "frac": max(frame_roof_ms, hbm_ms) / ms if ms > 0 else None,
+                  "hbm_peak_gbs": peaks["hbm_gbs"]}
     cb = None
     if world == 1 and not args.no_cpu:
         cb = cpu_baseline([synth.make_frame(args.config, 20000 + i) for i in range(3)], budget_s=20.0)
@@ -349,6 +359,7 @@ def main():
                    "parallelism": f"seed-sharded x{world} ({args.backend})" if sharded else f"replicas x{world}"},
         "roofline": roof,
         "frame_level_frac": frame_roof_ms / ms if ms > 0 else None,
+        "job_roofline": roof_terms,
         "seed_iters_per_frame": totals["seed_iters"] / max(1, totals["frames"]),
         "gpu_launches": totals["launches"],
         "clocks": clk.summary(),
