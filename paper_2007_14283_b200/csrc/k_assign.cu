@@ -19,6 +19,8 @@
 //   * warps 2-17: four groups of 4 warps (one per TMEM lane quarter) take the tiles round robin;
 //                the per-pixel argmax is a dependent scan, so it needs the thread parallelism.
 // Frames with more than 128 centres are left to the CUDA-core kernel (assign_kernel in k_post.cu).
+#include <type_traits>
+
 #include "fms_device.cuh"
 
 namespace fms {
@@ -267,19 +269,22 @@ __global__ void __launch_bounds__(kAsgThreads, 1) assign_tc_kernel(const __grid_
         uint32_t v[64];
         tmem_ld64(dbase + c0, v);
         tmem_ld_wait();
-        if (Kc - c0 >= 64) {
+        // only the 16-column groups that hold centres (compile-time bodies: v stays in registers);
+        // columns past Kc in the last group read as -inf
+        const int nk = min(64, Kc - c0);
+        auto scan = [&](auto groups) {
+          constexpr int G16 = decltype(groups)::value;
 #pragma unroll
-          for (int k = 0; k < 64; ++k) {
-            const float dv = __uint_as_float(v[k]);
+          for (int k = 0; k < 16 * G16; ++k) {
+            const float dv = (k < 16 * (G16 - 1) || k < nk) ? __uint_as_float(v[k]) : -INFINITY;
             if (dv > bv[k & 3]) { bv[k & 3] = dv; bl[k & 3] = c0 + k; }
           }
-        } else {
-          const int nk = Kc - c0;
-#pragma unroll
-          for (int k = 0; k < 64; ++k) {
-            const float dv = k < nk ? __uint_as_float(v[k]) : -INFINITY;
-            if (dv > bv[k & 3]) { bv[k & 3] = dv; bl[k & 3] = c0 + k; }
-          }
+        };
+        switch ((nk + 15) >> 4) {
+          case 1: scan(std::integral_constant<int, 1>{}); break;
+          case 2: scan(std::integral_constant<int, 2>{}); break;
+          case 3: scan(std::integral_constant<int, 3>{}); break;
+          default: scan(std::integral_constant<int, 4>{}); break;
         }
       }
       float best = bv[0];
