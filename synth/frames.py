@@ -153,3 +153,47 @@ def make_blobs(n: int, seed: int, D: int = 18, k: int = 10, std: float = 0.01):
     truth = rng.permutation(np.arange(n) % k).astype(np.int32)
     x = dirs[truth] + std * rng.standard_normal((n, D))
     return np.ascontiguousarray(x, dtype=np.float32), truth
+
+
+def make_stack(T: int, seed: int, H: int = 512, W: int = 512, D: int = 16, cells: int = 30,
+               radius=(20, 35), sigma: float = 0.02, drift_px: float = 0.5, turn_rad: float = 0.005):
+    """C5 (BASELINE configs[4]): a temporal stack of T frames clustered jointly
+    (tracking-style embeddings: one direction per cell track).  Cells drift by ~drift_px per frame
+    and each track's embedding direction random-walks by ~turn_rad radians per frame; background and
+    soft boundaries as in C2.  Returns (emb float32 [T*H*W, D], truth int32 [T*H*W]) in frame-major
+    raster order."""
+    rng = np.random.default_rng(np.random.SeedSequence([int(seed), 5555, T, H, W]))
+    cfg = dict(H=H, W=W, D=D, cells=cells, radius=radius, sigma=sigma, boundary="soft", gap=0)
+    dirs = _directions(rng, cells + 1, D)
+    discs = _discs(rng, cfg, hard=False)
+    vel = rng.normal(0.0, drift_px, size=(cells, 2))
+    n = H * W
+    emb = np.empty((T * n, D), dtype=np.float32)
+    truth = np.empty(T * n, dtype=np.int32)
+    yy, xx = np.mgrid[0:H, 0:W]
+    for t in range(T):
+        v = np.tile(dirs[0], (n, 1)).reshape(H, W, D)
+        tr = np.zeros((H, W), dtype=np.int32)
+        for k, (cy, cx, R) in enumerate(discs, start=1):
+            cy_t = np.clip(cy + vel[k - 1, 0] * t, R + 1, H - R - 1)
+            cx_t = np.clip(cx + vel[k - 1, 1] * t, R + 1, W - R - 1)
+            y0, y1 = max(0, int(cy_t - R - 6)), min(H, int(cy_t + R + 7))
+            x0, x1 = max(0, int(cx_t - R - 6)), min(W, int(cx_t + R + 7))
+            dist = np.sqrt((yy[y0:y1, x0:x1] + 0.5 - cy_t) ** 2 + (xx[y0:y1, x0:x1] + 0.5 - cx_t) ** 2)
+            a = 1.0 / (1.0 + np.exp(-(R - dist) / 0.7))
+            blk = v[y0:y1, x0:x1]
+            v[y0:y1, x0:x1] = (1.0 - a)[..., None] * blk + (4.0 * a)[..., None] * dirs[k]
+            tr[y0:y1, x0:x1][a > 0.5] = k
+        v = v.reshape(n, D)
+        v /= np.sqrt(np.sum(v * v, axis=1, keepdims=True))
+        x = v + sigma * np.clip(rng.standard_normal((n, D)), -3.0, 3.0)
+        x /= np.sqrt(np.sum(x * x, axis=1, keepdims=True))
+        emb[t * n:(t + 1) * n] = x
+        truth[t * n:(t + 1) * n] = tr.reshape(n)
+        # random-walk the track directions (small rotation towards a random orthogonal direction)
+        for k in range(1, cells + 1):
+            g = rng.standard_normal(D)
+            g -= (g @ dirs[k]) * dirs[k]
+            g /= np.sqrt(np.sum(g * g))
+            dirs[k] = np.cos(turn_rad) * dirs[k] + np.sin(turn_rad) * g
+    return emb, truth

@@ -149,6 +149,13 @@ def test_more_than_128_modes_exact():
     assert ro.K > 128 and max(ro.trace["round_Kc"]) > 128
 
 
+def test_c5_small_stack_ari():
+    """C5-shaped joint clustering of a temporal stack (tracks drift and their directions random-walk)
+    at a size the oracle finishes: 6 frames of 128x128, 8 tracks."""
+    emb, _ = synth.make_stack(6, seed=2, H=128, W=128, cells=8, radius=(10, 18))
+    check_near(emb, rng_seed=0, min_instance_px=6 * min_instance_px(128 * 128), saturation_stop=1)
+
+
 @pytest.mark.parametrize("n,kind", [(1000, 2), (2000, 2), (5000, 1)])
 def test_table1_blobs_exact(n, kind):
     """NEXT-3: the paper's Table 1 simulation data (18-D blobs, 10 orthogonal/opposite
