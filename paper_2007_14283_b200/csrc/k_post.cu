@@ -14,6 +14,8 @@
 //     I = #other clusters with >= min_instance_px pixels, r = 1 - |bg|/n,
 //     N_min = ceil( ln(1 - e^{ln P / I}) / ln(1 - r/I) ); stop when coverage holds
 //     (no candidates / total >= L N_min / total >= n / max_rounds / saturation), else double N.
+#include <cub/device/device_segmented_radix_sort.cuh>
+
 #include "fms_device.cuh"
 
 namespace fms {
@@ -26,31 +28,25 @@ __device__ __forceinline__ float dotv(const float* a, const float* b) {
   return s;
 }
 
-constexpr int kKeptSm = 256;  // kept centres cached in SMEM during the greedy scan
+constexpr int kKeptSm = 256;    // kept centres cached in SMEM during the greedy scan
+constexpr int kMergeSm = 8192;  // pools up to this size are sorted in SMEM
 
+// 1. assemble the pool (previous centres, then this round's converged seeds in seed order) and its
+//    sort keys (intensity desc, origin asc); returns P (or -1 after flagging a capacity error)
 template <int DP>
-__global__ void __launch_bounds__(1024) merge_kernel(Params p) {
-  const int f = blockIdx.x;
+__device__ int merge_assemble(const Params& p, int f, unsigned long long* keys, int* vals, int P2, int* sm) {
   FrameCtl& c = p.ctl[f];
-  if (c.phase != PH_POST) return;
-  extern __shared__ uint8_t dsm[];
-  __shared__ int sm[33];
-  __shared__ unsigned s_supp;
-  __shared__ unsigned s_inb[32];  // in-batch conflicts: bit j of s_inb[i] = candidate j (< i) within rho
-  __shared__ int s_kept, s_err;
-
   const int Kc = c.Kc;
   const int K = c.K_r;
   const int P = Kc + c.n_conv;
   if (P > p.P_cap) {
     if (threadIdx.x == 0) { c.status = 5; c.phase = PH_ERROR; }
-    return;
+    return -1;
   }
   float* pool = p.pool + (size_t)f * p.P_cap * DP;
   int* pint = p.pint + (size_t)f * p.P_cap;
   int* porg = p.porg + (size_t)f * p.P_cap;
-  float* cent = p.cent + (size_t)f * p.C_cap * DP;
-  // 1. assemble the pool: previous centres, then this round's converged seeds (seed order)
+  const float* cent = p.cent + (size_t)f * p.C_cap * DP;
   for (int k = threadIdx.x; k < Kc; k += blockDim.x) {
     for (int q = 0; q < DP; ++q) pool[(size_t)k * DP + q] = cent[(size_t)k * DP + q];
     pint[k] = p.cint[(size_t)f * p.C_cap + k];
@@ -70,11 +66,6 @@ __global__ void __launch_bounds__(1024) merge_kernel(Params p) {
     }
     carry += tot;
   }
-  // 2. sort keys (intensity desc, origin asc) -- bitonic in SMEM
-  int P2 = 1;
-  while (P2 < P) P2 <<= 1;
-  unsigned long long* keys = reinterpret_cast<unsigned long long*>(dsm);
-  int* vals = reinterpret_cast<int*>(keys + P2);
   __syncthreads();
   for (int i = threadIdx.x; i < P2; i += blockDim.x) {
     if (i < P) {
@@ -86,26 +77,21 @@ __global__ void __launch_bounds__(1024) merge_kernel(Params p) {
     }
   }
   __syncthreads();
-  for (int k = 2; k <= P2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P2; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const bool up = (i & k) == 0;
-          const unsigned long long a = keys[i], b = keys[ixj];
-          if ((a > b) == up) {
-            keys[i] = b; keys[ixj] = a;
-            const int t = vals[i]; vals[i] = vals[ixj]; vals[ixj] = t;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  // 3. greedy NMS in batches of 32; batch candidates and the first kKeptSm kept centres live in
-  //    SMEM (after the sort buffers), so the serial in-batch chain never waits on global memory
-  float* cand = reinterpret_cast<float*>(vals + P2);            // [32][DP]
-  float* keptv = cand + 32 * DP;                                 // [kKeptSm][DP]
+  return P;
+}
+
+// 3. greedy NMS in sorted order, in batches of 32; batch candidates and the first kKeptSm kept
+//    centres live in SMEM, so the serial in-batch chain never waits on global memory
+template <int DP>
+__device__ void merge_nms(const Params& p, int f, const int* vals, int P, float* cand, float* keptv) {
+  FrameCtl& c = p.ctl[f];
+  __shared__ unsigned s_supp;
+  __shared__ unsigned s_inb[32];  // in-batch conflicts: bit j of s_inb[i] = candidate j (< i) within rho
+  __shared__ int s_kept, s_err;
+  const float* pool = p.pool + (size_t)f * p.P_cap * DP;
+  const int* pint = p.pint + (size_t)f * p.P_cap;
+  const int* porg = p.porg + (size_t)f * p.P_cap;
+  float* cent = p.cent + (size_t)f * p.C_cap * DP;
   const float thr = p.rho_f;  // keep unless x.c >= 1 - rho
   if (threadIdx.x == 0) { s_kept = 0; s_err = 0; }
   __syncthreads();
@@ -167,6 +153,65 @@ __global__ void __launch_bounds__(1024) merge_kernel(Params p) {
   }
 }
 
+// pools up to kMergeSm: one CTA per frame, bitonic sort of the keys in SMEM
+template <int DP>
+__global__ void __launch_bounds__(1024) merge_kernel(Params p) {
+  const int f = blockIdx.x;
+  if (p.ctl[f].phase != PH_POST) return;
+  extern __shared__ uint8_t dsm[];
+  __shared__ int sm[33];
+  int P2 = 1;
+  while (P2 < p.ctl[f].Kc + p.ctl[f].n_conv) P2 <<= 1;
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(dsm);
+  int* vals = reinterpret_cast<int*>(keys + P2);
+  const int P = merge_assemble<DP>(p, f, keys, vals, P2, sm);
+  if (P < 0) return;
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const unsigned long long a = keys[i], b = keys[ixj];
+          if ((a > b) == up) {
+            keys[i] = b; keys[ixj] = a;
+            const int t = vals[i]; vals[i] = vals[ixj]; vals[ixj] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  float* cand = reinterpret_cast<float*>(vals + P2);  // [32][DP]
+  merge_nms<DP>(p, f, vals, P, cand, cand + 32 * DP);
+}
+
+// larger pools (Alg. 1 merges a mode per pixel): keys in global memory, a CUB segmented radix sort
+// between the two kernels
+template <int DP>
+__global__ void __launch_bounds__(1024) merge_pool_kernel(Params p) {
+  const int f = blockIdx.x;
+  if (p.ctl[f].phase != PH_POST) {
+    for (int i = threadIdx.x; i < p.P_cap; i += blockDim.x) {
+      p.mkeys[(size_t)f * p.P_cap + i] = ~0ull;
+      p.mvals[(size_t)f * p.P_cap + i] = -1;
+    }
+    return;
+  }
+  __shared__ int sm[33];
+  const int P = merge_assemble<DP>(p, f, p.mkeys + (size_t)f * p.P_cap, p.mvals + (size_t)f * p.P_cap, p.P_cap, sm);
+  (void)P;  // P < 0: capacity error flagged (phase ERROR), the NMS kernel skips the frame
+}
+
+template <int DP>
+__global__ void __launch_bounds__(1024) merge_nms_kernel(Params p) {
+  const int f = blockIdx.x;
+  FrameCtl& c = p.ctl[f];
+  if (c.phase != PH_POST) return;
+  __shared__ float cand[32 * DP];
+  __shared__ float keptv[kKeptSm * DP];
+  merge_nms<DP>(p, f, p.mvals_sorted + (size_t)f * p.P_cap, c.Kc + c.n_conv, cand, keptv);
+}
 
 template <int DP>
 __global__ void __launch_bounds__(256) assign_kernel(Params p) {
@@ -318,11 +363,36 @@ cudaError_t setup_post_attrs(int P_cap) {
 
 cudaError_t launch_assign_tc(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st);
 
+size_t merge_sort_temp_bytes(const Params& p) {
+  size_t bytes = 0;
+  cub::DeviceSegmentedRadixSort::SortPairs(nullptr, bytes, (const unsigned long long*)nullptr,
+                                          (unsigned long long*)nullptr, (const int*)nullptr, (int*)nullptr,
+                                          (int)((size_t)p.B * p.P_cap), p.B, (const int*)nullptr, (const int*)nullptr);
+  return bytes;
+}
+
+__global__ void merge_offsets_kernel(Params p) {
+  for (int f = threadIdx.x; f <= p.B; f += blockDim.x) p.moffs[f] = f * p.P_cap;
+}
+
 cudaError_t launch_post(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st) {
-  const int sm = merge_smem_bytes(p.P_cap, p.DP);
   const dim3 ga(16, p.B);
-  if (p.DP == 16) merge_kernel<16><<<p.B, 1024, sm, st>>>(p);
-  else merge_kernel<32><<<p.B, 1024, sm, st>>>(p);
+  if (p.P_cap <= kMergeSm) {
+    const int sm = merge_smem_bytes(p.P_cap, p.DP);
+    if (p.DP == 16) merge_kernel<16><<<p.B, 1024, sm, st>>>(p);
+    else merge_kernel<32><<<p.B, 1024, sm, st>>>(p);
+  } else {
+    if (p.DP == 16) merge_pool_kernel<16><<<p.B, 1024, 0, st>>>(p);
+    else merge_pool_kernel<32><<<p.B, 1024, 0, st>>>(p);
+    merge_offsets_kernel<<<1, 256, 0, st>>>(p);
+    size_t tb = p.msort_bytes;
+    cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairs(p.msort_temp, tb, p.mkeys, p.mkeys_sorted, p.mvals,
+                                                             p.mvals_sorted, (int)((size_t)p.B * p.P_cap), p.B,
+                                                             p.moffs, p.moffs + 1, 0, 64, st);
+    if (e != cudaSuccess) return e;
+    if (p.DP == 16) merge_nms_kernel<16><<<p.B, 1024, 0, st>>>(p);
+    else merge_nms_kernel<32><<<p.B, 1024, 0, st>>>(p);
+  }
   cudaError_t e = launch_assign_tc(p.DP, tm, p, num_sms, st);  // frames with <= 128 centres
   if (e != cudaSuccess) return e;
   if (p.DP == 16) assign_kernel<16><<<ga, 256, 0, st>>>(p);    // the rest

@@ -39,6 +39,7 @@ cudaError_t setup_assign_attrs();
 cudaError_t launch_output(const Params& p, float* centres_out, int cap, cudaStream_t st);
 cudaError_t setup_iter_attrs();
 cudaError_t setup_post_attrs(int P_cap);
+size_t merge_sort_temp_bytes(const Params& p);
 }  // namespace fms
 
 using namespace fms;
@@ -168,6 +169,15 @@ size_t carve(Params& p, uint8_t* base) {
   p.sample = (unsigned long long*)take(B * (size_t)p.sample_cap * 8);
   p.blkcnt = (int*)take(B * (size_t)p.nblk * 4);
   p.ctl = (FrameCtl*)take(B * sizeof(FrameCtl));
+  if (p.P_cap > kMaxPcap) {  // merge pool sorted in global memory (Alg. 1)
+    p.mkeys = (unsigned long long*)take(B * (size_t)p.P_cap * 8);
+    p.mkeys_sorted = (unsigned long long*)take(B * (size_t)p.P_cap * 8);
+    p.mvals = (int*)take(B * (size_t)p.P_cap * 4);
+    p.mvals_sorted = (int*)take(B * (size_t)p.P_cap * 4);
+    p.moffs = (int*)take((size_t)(B + 1) * 4);
+    p.msort_bytes = merge_sort_temp_bytes(p);
+    p.msort_temp = take(p.msort_bytes + 16);
+  }
   if (p.world > 1) {  // seed-sharding exchange buffers
     p.xchg = (int*)take((size_t)B * 4 * 4);
     p.xbuf = (int*)take((size_t)B * p.S_cap * (p.DP + 2) * 4);
@@ -202,7 +212,10 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   p.S_cap = (int)S;
   p.S_pad = (int)align_up((size_t)S, kBM);
   p.C_cap = (int)std::min<long long>(n, 65536);
-  p.P_cap = (int)std::min<long long>((long long)p.C_cap + p.S_cap, kMaxPcap);
+  // the merge pool holds the previous centres plus one round's converged seeds: bounded by the SMEM
+  // sort for the seeding policies; Alg. 1 (every pixel a seed) merges n modes in global memory
+  p.P_cap = pol->kind == FMS_SEEDS_ALL ? (int)std::min<long long>((long long)p.C_cap + p.S_cap, INT32_MAX / 2)
+                                       : (int)std::min<long long>((long long)p.C_cap + p.S_cap, kMaxPcap);
   p.tiles_cap = B * (p.S_pad / kBM);
   p.n_chunks = (p.n_ptiles + kChunkTiles - 1) / kChunkTiles;
   p.items_cap = p.tiles_cap * p.n_chunks;

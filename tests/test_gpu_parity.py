@@ -156,7 +156,7 @@ def test_c5_small_stack_ari():
     check_near(emb, rng_seed=0, min_instance_px=6 * min_instance_px(128 * 128), saturation_stop=1)
 
 
-@pytest.mark.parametrize("n,kind", [(1000, 2), (2000, 2), (5000, 1)])
+@pytest.mark.parametrize("n,kind", [(1000, 2), (2000, 2), (5000, 1), (9000, 2)])
 def test_table1_blobs_exact(n, kind):
     """NEXT-3: the paper's Table 1 simulation data (18-D blobs, 10 orthogonal/opposite
     clusters, noise 0.01) under Alg. 1 (kind 2, every point a seed) and OSOP: exact vs the oracle."""

@@ -40,9 +40,8 @@ def main():
     for i, n in enumerate(SIZES):
         emb, truth = synth.make_blobs(n, seed=0)
         x = torch.from_numpy(emb).cuda()
-        pols = [("OSOP (Alg. 2)", fms.default_policy(has_background=0))]
-        if n <= 8000:  # Alg. 1 merges every point's mode: the SMEM merge pool holds 8192 (kMaxPcap)
-            pols.insert(0, ("ALL (Alg. 1)", fms.default_policy(kind=fms.SEEDS_ALL)))
+        pols = [("ALL (Alg. 1)", fms.default_policy(kind=fms.SEEDS_ALL)),
+                ("OSOP (Alg. 2)", fms.default_policy(has_background=0))]
         for name, pol in pols:
             fms.cluster(x, policy=pol, centres_cap=64)
             times = []
