@@ -127,6 +127,27 @@ void fms_session_destroy(void* session);
 typedef int (*fms_exchange_fn)(void* user, int32_t* buf, int64_t count, void* stream);
 fms_status fms_set_exchange(void* ctx, fms_exchange_fn fn, void* user, int32_t rank, int32_t world);
 
+/* Pixel sharding (for frames or stacks too large for one GPU).  Every window sum of
+ * the lockstep iteration is a sum over pixels (Eq. 8 gated by Eq. 11, Alg. 2 l.4-9, PAPER.md
+ * P:137-139), and so are the mode intensities, the label histogram that feeds I and r of
+ * Eq. 19 and the coverage count of the OSOP stop rule, so a frame's pixels can be
+ * split over GPUs that each hold a contiguous range.  With world > 1 this rank holds pixels
+ * [offset, offset + n) of frames of n_global pixels: the clustering entry points then take n = this
+ * rank's pixel count and `emb`/`labels` of this rank's rows only ([B][n][d] / [B][n]); seeds,
+ * centres, K and the OSOP control are replicated, and every rank returns the same centres and K.
+ * Seed origins (and so the merge order and the selection keys of R11) use the global pixel index,
+ * so the result is identical to clustering the whole frame on one GPU.  The library calls `fn` (same
+ * contract as fms_set_exchange: in-place elementwise int32 sum over all ranks on `stream`) after K1
+ * (status), after each selection (the seed rows), after every K2 launch (the exact window sums G as
+ * split int64, and counts), and after each assignment (histogram, candidate count, coverage bits).
+ * Ranges of different ranks must be disjoint and cover [0, n_global); all ranks pass the same B,
+ * d and parameters.  world = 1 disables it.  Seed sharding and pixel sharding are exclusive: enabling
+ * one (world > 1) disables the other.  Errors: FMS_E_INVALID for rank/world out of range, a NULL fn
+ * with world > 1, n_global outside [1, 2^31) or offset outside [0, n_global) (and, at the clustering
+ * call, offset + n > n_global); a nonzero return of fn fails the call with FMS_E_NCCL. */
+fms_status fms_set_pixel_shard(void* ctx, fms_exchange_fn fn, void* user, int32_t rank, int32_t world,
+                               int64_t n_global, int64_t offset);
+
 /* Options: "profile_iter" (0/1): time every K2 launch with CUDA events for fms_run_stats.iter_ms.
  *          "poll_steps" (1..64, default 4): lockstep steps launched between two host polls of the
  *          device counters (a frame that finishes early idles at most poll_steps - 1 steps). */

@@ -15,7 +15,7 @@ MAX_ROUNDS = 16
 STATUS = {0: "OK", 2: "INVALID", 3: "ZERO_NORM", 4: "STALLED", 5: "CAPACITY", 6: "CUDA", 7: "NCCL", 8: "OOM",
           9: "INTERNAL"}
 EXPORTS = ["fms_default_policy", "fms_ctx_create", "fms_ctx_destroy", "fms_last_error", "fms_version",
-           "fms_set_option", "fms_set_exchange", "fms_cluster", "fms_cluster_batch", "fms_cluster_batch_host",
+           "fms_set_option", "fms_set_exchange", "fms_set_pixel_shard", "fms_cluster", "fms_cluster_batch", "fms_cluster_batch_host",
            "fms_session_create", "fms_session_step", "fms_session_seeds", "fms_session_destroy"]
 
 # int (*)(void* user, int32_t* buf, int64_t count, void* stream): in-place int32 sum over ranks
@@ -82,6 +82,7 @@ def lib() -> C.CDLL:
         L.fms_ctx_destroy.restype = None
         L.fms_set_option.argtypes = [vp, C.c_char_p, i64]
         L.fms_set_exchange.argtypes = [vp, EXCHANGE_FN, vp, i32, i32]
+        L.fms_set_pixel_shard.argtypes = [vp, EXCHANGE_FN, vp, i32, i32, i64, i64]
         L.fms_session_create.argtypes = [vp, C.POINTER(Policy), C.POINTER(vp)]
         L.fms_session_create.restype = C.c_int
         L.fms_session_step.argtypes = [vp, vp, i64, i32] + [f64, i32, f64, vp, vp, i32, vp, vp, C.POINTER(RunStats), vp]
@@ -94,7 +95,8 @@ def lib() -> C.CDLL:
         L.fms_cluster.argtypes = [vp, vp, i64, i32] + common
         L.fms_cluster_batch.argtypes = [vp, vp, i32, i64, i32] + common
         L.fms_cluster_batch_host.argtypes = [vp, vp, i32, i64, i32] + common
-        for fn in ("fms_default_policy", "fms_ctx_create", "fms_set_option", "fms_set_exchange", "fms_cluster",
+        for fn in ("fms_default_policy", "fms_ctx_create", "fms_set_option", "fms_set_exchange",
+                   "fms_set_pixel_shard", "fms_cluster",
                    "fms_cluster_batch", "fms_cluster_batch_host"):
             getattr(L, fn).restype = C.c_int
         _lib = L
@@ -156,6 +158,25 @@ class Context:
                     return 1
             self._xfn = EXCHANGE_FN(_cb)  # kept alive with the context
         self._check(lib().fms_set_exchange(self.h, self._xfn, None, int(rank), int(world)))
+
+    def _wrap_exchange(self, fn):
+        if fn is None:
+            return EXCHANGE_FN()
+
+        def _cb(user, buf, count, stream, _fn=fn):
+            try:
+                return int(_fn(buf, count, stream or 0))
+            except Exception as e:  # a Python exception must not unwind through the C library
+                self._xerr = e
+                return 1
+        return EXCHANGE_FN(_cb)
+
+    def set_pixel_shard(self, fn, rank: int, world: int, n_global: int, offset: int):
+        """Pixel sharding (include/fms.h fms_set_pixel_shard): this rank holds pixels
+        [offset, offset + n) of frames of n_global pixels; fn as in set_exchange."""
+        self._pfn = self._wrap_exchange(fn)  # kept alive with the context
+        self._check(lib().fms_set_pixel_shard(self.h, self._pfn, None, int(rank), int(world), int(n_global),
+                                              int(offset)))
 
     def _check(self, rc: int, allow=()):
         if rc != 0 and rc not in allow:

@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kAsgThreads, 1) assign_tc_kernel(const __grid_
     };
     auto flag_of = [&](const Cur& c) -> uint8_t {
       const long long px = (long long)c.t * kBN + q * 32 + lane;
-      return px < p.n ? p.flags[(size_t)c.f * p.n + px] : 0;
+      return px < p.n ? p.flags[flag_at(p, c.f, px)] : 0;
     };
     // this group's next tile: the kAsgGroups-th active item after c
     auto next_mine = [&](Cur c) -> Cur {
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kAsgThreads, 1) assign_tc_kernel(const __grid_
       if (px < p.n) {
         const size_t pi = (size_t)f * p.n + px;
         const bool covered = best >= tau2;
-        p.flags[pi] = (uint8_t)((fl & ~PF_COVERED) | (covered ? PF_COVERED : 0));
+        p.flags[flag_at(p, f, px)] = (uint8_t)((fl & ~PF_COVERED) | (covered ? PF_COVERED : 0));
         p.labels[pi] = lab;
         // warp-aggregated histogram: neighbouring pixels mostly share a label, and 32 same-address
         // shared atomics would serialise

@@ -13,8 +13,9 @@
 //     2^11 C = s_hi.hi + (s_hi 2^-11).lo + s_lo.hi        (three kind::f16 MMAs, fp32 accumulate)
 // decides the window with ~1e-7 error (plain fp16 would err by ~1e-4 and flip decisions), and
 //     2^11 G = W.hi + 2^-11 W.lo                          (N = 2 DP MMAs over [hi | lo])
-// is EXACT: 0/1 weights times integers |v| <= 2048 summed over <= 2^13 pixels stay below 2^24 in
-// fp32.  Exact sums make the result independent of how pixels are split across CTAs, so work is
+// is EXACT: the in-window weight is 2^-17 (an fp16 subnormal, see flat_kernel_pair), and 2^-17 times
+// integers |v| <= 2048 summed over <= 2^13 pixels are multiples of 2^-17 below 2^7 -- within fp32's
+// 24-bit significand.  Exact sums make the result independent of how pixels are split across CTAs, so work is
 // balanced freely and CTAs merge with fp64 atomics (integer-valued, hence order-independent).
 //
 // Structure (fused-attention style; the S x N weight matrix never leaves the SM):
@@ -69,21 +70,21 @@ struct IterCfg {
   static constexpr int SMEM = 1024 /*align slack*/ + 2 * 3 * A_B + STAGES * 2 * TILE_B + GS_B + 1024 /*barriers*/;
 };
 
-// In-window weights of two pixels -> packed fp16 pair of {0, 1.75}, low half = first pixel.
+// In-window weights of two pixels -> packed fp16 pair of {0, 2^-17}, low half = first pixel.
 // C and tau are 2^11-scaled fp32 numbers in [1024, 2048) near the threshold, so c - tau_m (tau_m =
 // the float just below tau) is an exact multiple of 2^-13 and
 //     sat(8192 c - 8192 tau_m) = [c >= tau]            (one FFMA.SAT, exact, inclusive: R5)
-// The byte permute takes the top byte of each 1.0f / 0.0f (0x3F / 0x00) over a zero byte: fp16
-// 0x3F00 = 1.75 or 0.  The weighted sums carry the factor 1.75 exactly (see the drain); the FMA
-// pipe does the compare and a single ALU op per pair packs.
+// The byte permute puts byte 2 of each 1.0f / 0.0f (0x80 / 0x00) over a zero byte: fp16 0x0080 =
+// 2^-17 (subnormal) or 0.  A power of two keeps the weighted sums exact in fp32 (see the header);
+// the drain scales by 2^17.  The FMA pipe does the compare and a single ALU op per pair packs.
 __device__ __forceinline__ uint32_t flat_kernel_pair(float c0, float c1, float k_tau) {
   const float w0 = __saturatef(__fmaf_rn(c0, 8192.0f, k_tau));
   const float w1 = __saturatef(__fmaf_rn(c1, 8192.0f, k_tau));
   uint32_t m;
-  asm("prmt.b32 %0, %1, %2, 0x7430;" : "=r"(m) : "r"(__float_as_uint(w0)), "r"(__float_as_uint(w1)));
+  asm("prmt.b32 %0, %1, %2, 0x4602;" : "=r"(m) : "r"(__float_as_uint(w0)), "r"(__float_as_uint(w1)));
   return m;
 }
-constexpr double kPScale = 1.75;  // value of an in-window weight
+constexpr double kPScale = 1.0 / 131072.0;  // value of an in-window weight, 2^-17
 
 // Timing experiments (tools/iter_probe.cu): -DFMS_K2_VARIANT=bits switches parts of the kernel off
 // (1 weighted-sum MMAs, 2 weight stores, 8/12 similarity MMAs, 16 C loads, 64 pixel loads), -DFMS_K2_TIMELINE logs a clock64 timeline of CTA 0.  The production
@@ -341,8 +342,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         double* dst = p.gacc + ((size_t)w.f * p.S_pad + (size_t)w.tile * kBM + row) * DP;
 #pragma unroll
         for (int k = 0; k < DP; ++k) {
-          // sums of weights 1.75 times integers (multiples of 2^-11) are exact in fp64, and dividing
-          // an exact multiple of 1.75 by 1.75 is exact (correctly rounded, representable quotient)
+          // exact sums of multiples of 2^-28 in fp64; dividing by the power of two 2^-17 is exact
           if (gs[k * kBM] != 0.0) atomicAdd(dst + k, gs[k * kBM] / kPScale);
           gs[k * kBM] = 0.0;
         }
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
           tmem_st_wait();
         } else {
 #pragma unroll
-          for (int i = 0; i < kColsPerWarp / 2; ++i) cnt += __popc(pk[i] & 0x01000100u);  // bit 8 of 0x3F00
+          for (int i = 0; i < kColsPerWarp / 2; ++i) cnt += __popc(pk[i] & 0x00800080u);  // bit 7 of 0x0080
         }
         tlog(p, lrole, ctile, 3);
         tc_fence_before();

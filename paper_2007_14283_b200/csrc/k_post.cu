@@ -257,8 +257,8 @@ __global__ void __launch_bounds__(256) assign_kernel(Params p) {
   if (valid) {
     const size_t pi = (size_t)f * p.n + i;
     const bool covered = best * p.inv[pi] >= p.tau_f;
-    const uint8_t fl = p.flags[pi];
-    p.flags[pi] = (uint8_t)((fl & ~PF_COVERED) | (covered ? PF_COVERED : 0));
+    const uint8_t fl = p.flags[flag_at(p, f, i)];
+    p.flags[flag_at(p, f, i)] = (uint8_t)((fl & ~PF_COVERED) | (covered ? PF_COVERED : 0));
     p.labels[pi] = lab;
     cand = (!covered && !(fl & PF_VISITED)) ? 1 : 0;
   }
@@ -301,7 +301,7 @@ __global__ void osop_kernel(Params p) {
           int I = 0;
           for (int k = 0; k < c.Kc; ++k)
             if (k != bg && hist[k] >= p.min_px) ++I;
-          const double rr = bg >= 0 ? 1.0 - (double)hist[bg] / (double)p.n : 1.0;
+          const double rr = bg >= 0 ? 1.0 - (double)hist[bg] / (double)p.n_glob : 1.0;
           double nmin = -1.0;  // -1 = infinite (no instance observed)
           if (I > 0 && rr > 0.0) {
             const double q = rr / (double)I;
@@ -315,7 +315,7 @@ __global__ void osop_kernel(Params p) {
           c.round_I[r] = I;
           c.round_r[r] = rr;
           c.round_nmin[r] = nmin;
-          const bool stop = c.ncand == 0 || c.total >= p.n || r + 1 >= p.max_rounds ||
+          const bool stop = c.ncand == 0 || c.total >= p.n_glob || r + 1 >= p.max_rounds ||
                             (nmin > 0.0 && (double)c.total >= p.L * nmin) ||
                             (p.sat_stop && r >= 1 && I <= c.I_prev);
           c.I_prev = I;
@@ -375,7 +375,14 @@ __global__ void merge_offsets_kernel(Params p) {
   for (int f = threadIdx.x; f <= p.B; f += blockDim.x) p.moffs[f] = f * p.P_cap;
 }
 
-cudaError_t launch_post(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st) {
+cudaError_t launch_osop(const Params& p, cudaStream_t st) {
+  osop_kernel<<<1, 1024, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// merge + assignment (+ the OSOP step unless `osop` is false: pixel sharding sums the histogram
+// over the ranks first)
+cudaError_t launch_post(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st, bool osop) {
   const dim3 ga(16, p.B);
   if (p.P_cap <= kMergeSm) {
     const int sm = merge_smem_bytes(p.P_cap, p.DP);
@@ -397,7 +404,7 @@ cudaError_t launch_post(const Params& p, const TMaps& tm, int num_sms, cudaStrea
   if (e != cudaSuccess) return e;
   if (p.DP == 16) assign_kernel<16><<<ga, 256, 0, st>>>(p);    // the rest
   else assign_kernel<32><<<ga, 256, 0, st>>>(p);
-  osop_kernel<<<1, 1024, 0, st>>>(p);
+  if (osop) osop_kernel<<<1, 1024, 0, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -54,7 +54,7 @@ __global__ void prep_kernel(Params p) {
 #pragma unroll
     for (int k = 0; k < DP; ++k) limbs(v[k] * inv, h[k], l[k]);
     p.inv[(size_t)f * p.n + i] = inv;
-    p.flags[(size_t)f * p.n + i] = 0;
+    p.flags[flag_at(p, f, i)] = 0;
   } else {
 #pragma unroll
     for (int k = 0; k < DP; ++k) h[k] = l[k] = __float2half_rn(0.f);
@@ -71,7 +71,7 @@ __global__ void prep_kernel(Params p) {
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ bool is_candidate(const Params& p, int f, int round, long long i) {
   if (round == 0) return true;
-  return (p.flags[(size_t)f * p.n + i] & (PF_VISITED | PF_COVERED)) == 0;
+  return (p.flags[(size_t)f * p.n_glob + i] & (PF_VISITED | PF_COVERED)) == 0;  // i: global index
 }
 
 __global__ void sel_prepare_kernel(Params p) {
@@ -82,8 +82,8 @@ __global__ void sel_prepare_kernel(Params p) {
   if (c.status != 0) { c.phase = PH_ERROR; return; }
   long long ncand, Kreq;
   if (c.round == 0) {
-    ncand = p.n;
-    Kreq = p.kind == 2 /*ALL*/ ? p.n : (long long)p.n_seeds;
+    ncand = p.n_glob;
+    Kreq = p.kind == 2 /*ALL*/ ? p.n_glob : (long long)p.n_seeds;
   } else {
     ncand = c.ncand;
     Kreq = c.K_next;
@@ -110,11 +110,11 @@ __global__ void sel_collect_kernel(Params p) {
   const int round = c.round;
   const unsigned long long T = c.thresh;
   const int lane = threadIdx.x & 31;
-  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < p.n; i0 += (long long)gridDim.x * blockDim.x) {
+  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < p.n_glob; i0 += (long long)gridDim.x * blockDim.x) {
     const long long i = i0 + threadIdx.x;
     bool take = false;
     unsigned long long key = 0;
-    if (i < p.n && is_candidate(p, f, round, i)) {
+    if (i < p.n_glob && is_candidate(p, f, round, i)) {
       key = sel_key(p.rng_seed, round, i);
       take = key < T;
     }
@@ -182,7 +182,7 @@ __global__ void sel_kth_kernel(Params p) {
   if (M >= K && M <= p.sample_cap) {
     kth = radix_kth(p, f, c.round, true, M, K);
   } else {
-    kth = radix_kth(p, f, c.round, false, p.n, K);  // rare: sample too small / overflowed
+    kth = radix_kth(p, f, c.round, false, p.n_glob, K);  // rare: sample too small / overflowed
   }
   if (threadIdx.x == 0) c.kth = kth;
 }
@@ -203,7 +203,7 @@ __global__ void sel_count_kernel(Params p) {
   int cnt = 0;
   for (int u = 0; u < kSelBlock / 256; ++u) {
     long long i = base + u * 256 + threadIdx.x;
-    if (i < p.n && is_selected(p, f, c, i)) ++cnt;
+    if (i < p.n_glob && is_selected(p, f, c, i)) ++cnt;
   }
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   __shared__ int ws[8];
@@ -212,7 +212,7 @@ __global__ void sel_count_kernel(Params p) {
   if (threadIdx.x == 0) {
     int s = 0;
     for (int w = 0; w < 8; ++w) s += ws[w];
-    p.blkcnt[(size_t)f * p.nblk + blockIdx.x] = s;
+    p.blkcnt[(size_t)f * p.nblk_glob + blockIdx.x] = s;
   }
 }
 
@@ -222,12 +222,12 @@ __global__ void sel_scan_kernel(Params p) {
   if (c.phase != PH_SELECT) return;
   __shared__ int sm[33];
   int carry = 0;
-  for (int b0 = 0; b0 < p.nblk; b0 += blockDim.x) {
+  for (int b0 = 0; b0 < p.nblk_glob; b0 += blockDim.x) {
     int b = b0 + threadIdx.x;
-    int v = b < p.nblk ? p.blkcnt[(size_t)f * p.nblk + b] : 0;
+    int v = b < p.nblk_glob ? p.blkcnt[(size_t)f * p.nblk_glob + b] : 0;
     int tot;
     int ex = block_excl_scan(v, sm, &tot);
-    if (b < p.nblk) p.blkcnt[(size_t)f * p.nblk + b] = carry + ex;
+    if (b < p.nblk_glob) p.blkcnt[(size_t)f * p.nblk_glob + b] = carry + ex;
     carry += tot;
   }
   if (threadIdx.x == 0 && carry != c.K_r) {
@@ -246,15 +246,19 @@ __global__ void sel_write_kernel(Params p) {
   unsigned sel = 0;
   for (int u = 0; u < 8; ++u) {
     long long i = base + u;
-    if (i < p.n && is_selected(p, f, c, i)) sel |= 1u << u;
+    if (i < p.n_glob && is_selected(p, f, c, i)) sel |= 1u << u;
   }
-  int pos = p.blkcnt[(size_t)f * p.nblk + blockIdx.x] + block_excl_scan(__popc(sel), sm, nullptr);
+  int pos = p.blkcnt[(size_t)f * p.nblk_glob + blockIdx.x] + block_excl_scan(__popc(sel), sm, nullptr);
   for (int u = 0; u < 8; ++u) {
     if (!(sel & (1u << u))) continue;
     const long long i = base + u;
     const size_t so = (size_t)f * p.S_cap + pos;
-    const float inv = p.inv[(size_t)f * p.n + i];
-    const float* x = p.emb + ((size_t)f * p.n + i) * p.d;
+    // pixel sharding: only the rank holding pixel i has its embedding; the others write a zero row
+    // and the seed rows are summed over the ranks before the round iterates (k_shard.cu)
+    const long long il = i - p.pix_off;
+    const bool have = il >= 0 && il < p.n;
+    const float inv = have ? p.inv[(size_t)f * p.n + il] : 0.f;
+    const float* x = p.emb + ((size_t)f * p.n + (have ? il : 0)) * p.d;
     float* s = p.seeds + so * DP;
     // the operand row (and accumulators) of an active seed sit at its compacted position; with seed
     // sharding only this rank's seeds (j % world == rank) are active here, at j / world
@@ -263,7 +267,7 @@ __global__ void sel_write_kernel(Params p) {
     __align__(16) __half sh[DP], ss[DP], sl[DP];
 #pragma unroll
     for (int k = 0; k < DP; ++k) {
-      float v = k < p.d ? x[k] * inv : 0.f;
+      float v = (have && k < p.d) ? x[k] * inv : 0.f;
       s[k] = v;
       split_seed(v, sh[k], ss[k], sl[k]);
     }
@@ -284,7 +288,7 @@ __global__ void sel_write_kernel(Params p) {
     p.sorig[so] = (int)i;
     p.sstat[so] = ST_ACTIVE;
     p.scnt[so] = 0;
-    p.flags[(size_t)f * p.n + i] |= PF_VISITED;
+    p.flags[(size_t)f * p.n_glob + i] |= PF_VISITED;
     ++pos;
   }
 }
@@ -327,16 +331,16 @@ cudaError_t launch_prep(const Params& p, cudaStream_t st) {
 
 cudaError_t launch_select(const Params& p, int num_sms, cudaStream_t st) {
   sel_prepare_kernel<<<(p.B + 127) / 128, 128, 0, st>>>(p);
-  int gx = (int)((p.n + 255) / 256);
+  int gx = (int)((p.n_glob + 255) / 256);
   int cap = (num_sms * 8 + p.B - 1) / p.B;
   if (gx > cap) gx = cap;
   if (gx < 1) gx = 1;
   sel_collect_kernel<<<dim3(gx, p.B), 256, 0, st>>>(p);
   sel_kth_kernel<<<p.B, 1024, 0, st>>>(p);
-  sel_count_kernel<<<dim3(p.nblk, p.B), 256, 0, st>>>(p);
+  sel_count_kernel<<<dim3(p.nblk_glob, p.B), 256, 0, st>>>(p);
   sel_scan_kernel<<<p.B, 1024, 0, st>>>(p);
-  if (p.DP == 16) sel_write_kernel<16><<<dim3(p.nblk, p.B), 256, 0, st>>>(p);
-  else sel_write_kernel<32><<<dim3(p.nblk, p.B), 256, 0, st>>>(p);
+  if (p.DP == 16) sel_write_kernel<16><<<dim3(p.nblk_glob, p.B), 256, 0, st>>>(p);
+  else sel_write_kernel<32><<<dim3(p.nblk_glob, p.B), 256, 0, st>>>(p);
   sel_finish_kernel<<<(p.B + 127) / 128, 128, 0, st>>>(p);
   return cudaGetLastError();
 }

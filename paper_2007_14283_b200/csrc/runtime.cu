@@ -29,7 +29,13 @@ cudaError_t launch_prep(const Params& p, cudaStream_t st);
 cudaError_t launch_select(const Params& p, int num_sms, cudaStream_t st);
 cudaError_t launch_plan(const Params& p, cudaStream_t st);
 cudaError_t launch_iter(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st);
-cudaError_t launch_post(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st);
+cudaError_t launch_post(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st, bool osop);
+cudaError_t launch_osop(const Params& p, cudaStream_t st);
+cudaError_t launch_pstat(const Params& p, bool pack, cudaStream_t st);
+cudaError_t launch_psel_kmax(const Params& p, cudaStream_t st);
+cudaError_t launch_psel(const Params& p, bool pack, cudaStream_t st);
+cudaError_t launch_pstep(const Params& p, bool pack, cudaStream_t st);
+cudaError_t launch_ppost(const Params& p, bool pack, cudaStream_t st);
 cudaError_t launch_update(const Params& p, int num_sms, cudaStream_t st);
 cudaError_t launch_ctl(const Params& p, cudaStream_t st);
 cudaError_t launch_xchg_pack(const Params& p, cudaStream_t st);
@@ -80,6 +86,13 @@ struct Ctx {
   fms_exchange_fn xfn = nullptr;
   void* xuser = nullptr;
   int rank = 0, world = 1;
+  // pixel sharding: the caller's int32 sum; this rank holds pixels [poff, poff + n) of n_glob
+  fms_exchange_fn pfn = nullptr;
+  void* puser = nullptr;
+  int prank = 0, pworld = 1;
+  long long pn_glob = 0, poff = 0;
+  void* pbuf = nullptr;  // exchange buffer, grown on demand
+  size_t pbuf_bytes = 0;
   int poll = kPoll;  // lockstep steps between host polls ("poll_steps")
 };
 
@@ -146,7 +159,7 @@ size_t carve(Params& p, uint8_t* base) {
   p.Xh = (__half*)take(B * p.n_pad * p.DP * 2);
   p.Xl = (__half*)take(B * p.n_pad * p.DP * 2);
   p.inv = (float*)take(B * p.n * 4);
-  p.flags = (uint8_t*)take(B * p.n);
+  p.flags = (uint8_t*)take(B * p.n_glob);
   p.seeds = (float*)take(B * (size_t)p.S_cap * p.DP * 4);
   p.sop = (__half*)take(B * (size_t)p.S_pad * p.DP * 2);
   p.sops = (__half*)take(B * (size_t)p.S_pad * p.DP * 2);
@@ -167,7 +180,7 @@ size_t carve(Params& p, uint8_t* base) {
   p.tiles = (TileTask*)take((size_t)p.tiles_cap * sizeof(TileTask));
   p.counters = (int*)take(kCounters * 4);
   p.sample = (unsigned long long*)take(B * (size_t)p.sample_cap * 8);
-  p.blkcnt = (int*)take(B * (size_t)p.nblk * 4);
+  p.blkcnt = (int*)take(B * (size_t)p.nblk_glob * 4);
   p.ctl = (FrameCtl*)take(B * sizeof(FrameCtl));
   if (p.P_cap > kMaxPcap) {  // merge pool sorted in global memory (Alg. 1)
     p.mkeys = (unsigned long long*)take(B * (size_t)p.P_cap * 8);
@@ -208,10 +221,20 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   p.n = n;
   p.n_pad = (long long)align_up((size_t)n, kBN);
   p.n_ptiles = (int)(p.n_pad / kBN);
-  long long S = pol->kind == FMS_SEEDS_FIXED ? std::min<long long>(pol->n_seeds, n) : n;
+  const bool pshard = c->pworld > 1;
+  if (pshard && (c->poff < 0 || c->poff + n > c->pn_glob))
+    return fail(c, FMS_E_INVALID, "pixel shard [offset, offset + n) outside the frame of n_global pixels");
+  p.n_glob = pshard ? c->pn_glob : n;
+  p.pix_off = pshard ? c->poff : 0;
+  p.pworld = pshard ? c->pworld : 1;
+  p.prank = pshard ? c->prank : 0;
+  p.nblk_glob = (int)((p.n_glob + 2047) / 2048);
+  p.pcov_words = (int)((p.n_glob + 31) / 32);
+  const long long ng = p.n_glob;
+  long long S = pol->kind == FMS_SEEDS_FIXED ? std::min<long long>(pol->n_seeds, ng) : ng;
   p.S_cap = (int)S;
   p.S_pad = (int)align_up((size_t)S, kBM);
-  p.C_cap = (int)std::min<long long>(n, 65536);
+  p.C_cap = (int)std::min<long long>(ng, 65536);
   // the merge pool holds the previous centres plus one round's converged seeds: bounded by the SMEM
   // sort for the seeding policies; Alg. 1 (every pixel a seed) merges n modes in global memory
   p.P_cap = pol->kind == FMS_SEEDS_ALL ? (int)std::min<long long>((long long)p.C_cap + p.S_cap, INT32_MAX / 2)
@@ -219,7 +242,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   p.tiles_cap = B * (p.S_pad / kBM);
   p.n_chunks = (p.n_ptiles + kChunkTiles - 1) / kChunkTiles;
   p.items_cap = p.tiles_cap * p.n_chunks;
-  p.sample_cap = (int)std::min<long long>(n, (long long)S + 8 * (long long)std::sqrt((double)S) + 1024);
+  p.sample_cap = (int)std::min<long long>(ng, (long long)S + 8 * (long long)std::sqrt((double)S) + 1024);
   p.nblk = (int)((n + 2047) / 2048);
   p.h = h;
   p.tau = 1.0 - h;
@@ -282,13 +305,61 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
     CU(cudaMemsetAsync(p.cacc, 0, (size_t)B * p.S_pad * 4, st));
     c->fresh_ws = false;
   }
+  auto pgrow = [&](size_t ints) -> fms_status {  // pixel-sharding exchange buffer
+    const size_t bytes = std::max<size_t>(ints, 1) * 4;
+    if (bytes > c->pbuf_bytes) {
+      CU(cudaStreamSynchronize(st));
+      if (c->pbuf) cudaFree(c->pbuf);
+      c->pbuf = nullptr;
+      c->pbuf_bytes = 0;
+      if (cudaMalloc(&c->pbuf, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, FMS_E_OOM, "pixel-shard exchange buffer allocation failed");
+      }
+      c->pbuf_bytes = bytes;
+    }
+    p.pbuf = reinterpret_cast<int*>(c->pbuf);
+    return FMS_OK;
+  };
+  auto pxchg = [&](size_t ints, const char* what) -> fms_status {
+    if (c->pfn(c->puser, p.pbuf, (int64_t)ints, st) != 0) return fail(c, FMS_E_NCCL, std::string(what) + " exchange failed");
+    return FMS_OK;
+  };
+  const size_t post_ints = (size_t)B * ((size_t)p.C_cap + 2 + p.pcov_words);
+  if (pshard) {
+    CU(cudaMemsetAsync(p.flags, 0, (size_t)B * p.n_glob, st));  // other ranks' pixels: filled by exchanges
+    fms_status g = pgrow(std::max<size_t>(post_ints, B));
+    if (g != FMS_OK) return g;
+  }
   CU(launch_prep(p, st));
+  if (pshard) {  // a zero-norm row on any rank fails the frame on every rank
+    CU(launch_pstat(p, true, st));
+    fms_status g = pxchg(B, "status");
+    if (g != FMS_OK) return g;
+    CU(launch_pstat(p, false, st));
+  }
   int steps = 0, launches = 0;
   long long kernels = 2;  // init + prep
   std::vector<int> prof_slots;
   for (int round = 0; round < pol->max_rounds + 1; ++round) {
     CU(launch_select(p, c->num_sms, st));
     kernels += 7;
+    if (pshard) {  // the round's seed rows come from the ranks holding the seed pixels
+      CU(launch_psel_kmax(p, st));
+      CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      p.pkmax = c->h_counters[8];
+      fms_status g = pgrow(std::max(post_ints, (size_t)B * p.pkmax * (2 * p.DP + 1)));
+      if (g != FMS_OK) return g;
+      if (p.pkmax > 0) {
+        CU(launch_psel(p, true, st));
+        g = pxchg((size_t)B * p.pkmax * p.DP, "seed");
+        if (g != FMS_OK) return g;
+        CU(launch_psel(p, false, st));
+        kernels += 2;
+      }
+      kernels += 1;
+    }
     for (int s = 0; s < max_iters + c->poll; s += c->poll) {
       for (int k = 0; k < c->poll; ++k) {
         CU(launch_plan(p, st));
@@ -321,6 +392,13 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
         } else {
           CU(launch_iter(p.DP, tm, p, c->num_sms, st));
         }
+        if (pshard && p.pkmax > 0) {  // window sums and counts over all pixels
+          CU(launch_pstep(p, true, st));
+          fms_status g = pxchg((size_t)B * p.pkmax * (2 * p.DP + 1), "step");
+          if (g != FMS_OK) return g;
+          CU(launch_pstep(p, false, st));
+          kernels += 2;
+        }
         CU(launch_update(p, c->num_sms, st));
         if (p.world > 1) {  // seed sharding: per-frame step counts summed over the ranks
           CU(launch_xchg_pack(p, st));
@@ -349,8 +427,16 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
       }
       kernels += 1;
     }
-    CU(launch_post(p, tm, c->num_sms, st));
+    CU(launch_post(p, tm, c->num_sms, st, !pshard));
     kernels += 4;  // merge, assign (tensor cores), assign (CUDA cores, > 256 centres), osop
+    if (pshard) {  // histogram, candidate count and coverage over all pixels before the OSOP step
+      CU(launch_ppost(p, true, st));
+      fms_status g = pxchg(post_ints, "round");
+      if (g != FMS_OK) return g;
+      CU(launch_ppost(p, false, st));
+      CU(launch_osop(p, st));
+      kernels += 2;
+    }
     CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (c->h_counters[2] == 0) break;  // every frame DONE (or in error)
@@ -472,6 +558,7 @@ void fms_ctx_destroy(void* ctx) {
   if (c->h_counters) cudaFreeHost(c->h_counters);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->h_prof) cudaFreeHost(c->h_prof);
+  if (c->pbuf) cudaFree(c->pbuf);
   for (auto e : c->ev) cudaEventDestroy(e);
   if (c->t0) cudaEventDestroy(c->t0);
   if (c->t1) cudaEventDestroy(c->t1);
@@ -492,7 +579,35 @@ fms_status fms_set_exchange(void* ctx, fms_exchange_fn fn, void* user, int32_t r
   c->xuser = user;
   c->rank = rank;
   c->world = world;
+  if (world > 1) {  // the two sharding modes are exclusive
+    c->pfn = nullptr;
+    c->pworld = 1;
+    c->prank = 0;
+  }
   c->fresh_ws = true;  // the carve changes (exchange buffers)
+  return FMS_OK;
+}
+
+fms_status fms_set_pixel_shard(void* ctx, fms_exchange_fn fn, void* user, int32_t rank, int32_t world,
+                               int64_t n_global, int64_t offset) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c) return FMS_E_INVALID;
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !fn))
+    return fail(c, FMS_E_INVALID, "need 0 <= rank < world and an exchange function when world > 1");
+  if (world > 1 && (n_global < 1 || n_global >= (1ll << 31) || offset < 0 || offset >= n_global))
+    return fail(c, FMS_E_INVALID, "need 1 <= n_global < 2^31 and 0 <= offset < n_global");
+  c->pfn = fn;
+  c->puser = user;
+  c->prank = rank;
+  c->pworld = world;
+  c->pn_glob = n_global;
+  c->poff = offset;
+  if (world > 1) {  // the two sharding modes are exclusive
+    c->xfn = nullptr;
+    c->world = 1;
+    c->rank = 0;
+  }
+  c->fresh_ws = true;
   return FMS_OK;
 }
 

@@ -1,5 +1,5 @@
-"""Seed sharding over torch.distributed: the exchange callback for
-Context.set_exchange.
+"""Seed sharding and pixel sharding (8(e)3) over torch.distributed: the exchange
+callback for Context.set_exchange / Context.set_pixel_shard.
 
 The library calls the exchange at its two collective points (per lockstep step: per-frame counts;
 per round: the owners' converged seeds) with an int32 device buffer and its stream; this module
@@ -50,3 +50,27 @@ def enable_seed_sharding(ctx, group=None):
     else:
         ctx.set_exchange(make_exchange(group), rank, world)
     return ctx
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous pixel range [lo, hi) of `rank` when n pixels are split over `world` ranks (sizes
+    differ by at most one; the first n % world ranks take one more)."""
+    if not (0 <= rank < world) or n < world:
+        raise ValueError("need 0 <= rank < world <= n")
+    q, r = divmod(n, world)
+    lo = rank * q + min(rank, r)
+    return lo, lo + q + (1 if rank < r else 0)
+
+
+def enable_pixel_sharding(ctx, n_global: int, group=None):
+    """Make `ctx` cluster frames of n_global pixels of which this rank holds shard_range(n_global, rank,
+    world): pass this rank's rows to the clustering calls; every rank returns the same centres and K,
+    and labels for its own rows.  Returns (lo, hi)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if world == 1:
+        ctx.set_pixel_shard(None, 0, 1, n_global, 0)
+        return 0, n_global
+    lo, hi = shard_range(n_global, rank, world)
+    ctx.set_pixel_shard(make_exchange(group), rank, world, n_global, lo)
+    return lo, hi
