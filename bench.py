@@ -6,7 +6,8 @@ metric: frames/sec clustering 512x512 frames of 16-D embeddings (BASELINE.json c
 step  : one call of fms_cluster_batch on a batch of B resident frames (every §8(a) row runs:
         normalise, select, lockstep iteration, intensity, merge, assign, OSOP control).
 multi-GPU: frames are independent (replicas, no data-path collective); each rank
-        clusters its own batches; the elapsed time is the max over ranks.
+        clusters its own batches; the elapsed time is the max over ranks.  N > 1 runs add two strong-
+        scaling measurements: C4 seed-sharded (8(e) 2) and the C5 stack pixel-sharded (8(e) 3).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl fms|reference]
 """
@@ -206,6 +207,57 @@ def seed_sharded_c4(world, rank, local, B=2, warmup=1, steps=3):
             "one_rank_value": steps * B / (single_ms / 1e3), "K_equal_to_one_rank": K1 == KN}
 
 
+def pixel_sharded_c5(world, rank, local, T=92, warmup=1, steps=3):
+    """SURVEY 8(e)3 / BASELINE configs[4]: the C5 temporal stack (T x 512x512, 16-D, ~30 tracks)
+    clustered jointly as one problem, its pixels split over the ranks (fms_set_pixel_shard: per
+    lockstep step an all-reduce of the exact window sums), next to the whole stack clustered by one
+    rank alone (strong scaling).  Device time, max over ranks; checks that K and this rank's labels
+    equal the one-rank run."""
+    import numpy as np
+    import torch
+
+    import paper_2007_14283_b200 as fms
+    import synth
+    from paper_2007_14283_b200.dist import enable_pixel_sharding
+    from synth.frames import min_instance_px
+    dev = torch.device("cuda", local)
+    emb, _ = synth.make_stack(T, seed=0)
+    n, d = emb.shape
+    pol = fms.default_policy(min_instance_px=min_instance_px(512 * 512) * T, saturation_stop=1)
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(ctx, x):
+        nl = x.shape[0]
+        labels = torch.empty((1, nl), dtype=torch.int32, device=dev)
+        cent = torch.empty((1, CAP, d), dtype=torch.float32, device=dev)
+        Ks = None
+        for _ in range(warmup):
+            ctx.cluster_batch_ptr(x.data_ptr(), 1, nl, d, labels.data_ptr(), cent.data_ptr(), CAP, H, MAX_ITERS,
+                                  None, pol, stream.cuda_stream)
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            _, Ks, _, _ = ctx.cluster_batch_ptr(x.data_ptr(), 1, nl, d, labels.data_ptr(), cent.data_ptr(), CAP, H,
+                                                MAX_ITERS, None, pol, stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return reduce_max(e0.elapsed_time(e1), world, dev), Ks, labels
+
+    xf = torch.from_numpy(emb).to(dev)
+    single_ms, K1, lab1 = timed(fms.Context(local), xf)
+    ctx = fms.Context(local)
+    lo, hi = enable_pixel_sharding(ctx, n)
+    xs = xf[lo:hi].contiguous()
+    sharded_ms, KN, labN = timed(ctx, xs)
+    same = bool(torch.equal(labN[0], lab1[0, lo:hi])) and K1 == KN
+    same = reduce_max(0.0 if same else 1.0, world, dev) == 0.0
+    return {"config": f"C5: {T} x 512x512 stack, 16-D, 30 tracks, joint clustering ({n} px)", "frames_per_step": T,
+            "n_gpus": world, "value": steps * T / (sharded_ms / 1e3), "unit": "frames/s", "scaling": "strong",
+            "one_rank_value": steps * T / (single_ms / 1e3), "equal_to_one_rank": same}
+
+
 def run_reference(args, world, rank):
     if rank != 0:  # the reference arm runs on rank 0 only; other ranks exit 0 without work
         return
@@ -310,12 +362,16 @@ def main():
         e2e = {"value": ksteps * B * (1 if sharded else world) / (ems / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": B * n * d * 4, "d2h_bytes_per_step": B * n * 4 + B * CAP * d * 4}
 
-    seed_sh = None
+    seed_sh = pix_sh = None
     if world > 1 and not sharded and not args.no_seed_shard:
         try:
             seed_sh = seed_sharded_c4(world, rank, local)
         except Exception as e:  # reported, not fatal: the replicas line above is the headline
             seed_sh = {"error": f"{type(e).__name__}: {e}"[:300]}
+        try:
+            pix_sh = pixel_sharded_c5(world, rank, local)
+        except Exception as e:
+            pix_sh = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     if rank != 0:
         if world > 1:
@@ -368,6 +424,8 @@ def main():
     }
     if seed_sh is not None:
         line["seed_sharded"] = seed_sh
+    if pix_sh is not None:
+        line["pixel_sharded"] = pix_sh
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
