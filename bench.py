@@ -319,7 +319,8 @@ def main():
     for k in range(args.warmup):
         step(k)
     ctx.set_option("profile_iter", 1)
-    totals = dict(iter_ms=0.0, iter_seed_iters=0, iter_launches=0, launches=0, frames=0, seed_iters=0)
+    totals = dict(iter_ms=0.0, iter_seed_iters=0, iter_count_units=0, iter_launches=0, launches=0, frames=0,
+                  seed_iters=0, assign_pairs=0)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -330,10 +331,12 @@ def main():
             fs, rs = step(k)
             totals["iter_ms"] += rs["iter_ms"]
             totals["iter_seed_iters"] += rs["iter_seed_iters"]
+            totals["iter_count_units"] += rs["iter_count_units"]
             totals["iter_launches"] += rs["iter_launches"]
             totals["launches"] += rs["launches"]
             totals["frames"] += B
             totals["seed_iters"] += sum(f["seed_iters"] for f in fs)
+            totals["assign_pairs"] += sum(sum(f["round_Kc"][:f["rounds"]]) for f in fs)
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = reduce_max(ev0.elapsed_time(ev1), world, dev)
@@ -378,7 +381,9 @@ def main():
             torch.distributed.destroy_process_group()
         return
     peaks, src = measured_peaks()
-    flops = totals["iter_seed_iters"] * n * 4 * d          # algorithmic: 4 n D per active seed-iteration
+    # algorithmic: 4 n D per active seed-iteration (similarity + weighted sum) and 2 n D
+    # per converged mode in K2's intensity pass (similarity only, R10)
+    flops = totals["iter_seed_iters"] * n * 4 * d + totals["iter_count_units"] * n * 2 * d
     achieved = flops / (totals["iter_ms"] / 1e3) / 1e12 if totals["iter_ms"] > 0 else None
     peak = peaks["bf16_tflops_sustained"]
     roof = {"bound": "tensor", "kernel": "fms::iter_kernel<16> (K2)", "achieved": achieved, "peak": peak,
@@ -389,15 +394,18 @@ def main():
             "iter_share_of_step": totals["iter_ms"] / ms if ms > 0 else None}
     # frame-level roofline: algorithmic iteration FLOPs of the whole job at the tensor peak
     frame_roof_ms = flops / (peak * 1e12) * 1e3
+    # + the assignment's contraction (2 n D per pixel-centre pair per round) for the job terms
+    job_flops = flops + totals["assign_pairs"] * n * 2 * d
+    job_tensor_ms = job_flops / (peak * 1e12) * 1e3
     # north_star / SURVEY 8(d): the job's roofline is the slowest of three limits -- contraction FLOPs
     # at the tensor peak, kernel exponentials at the SFU peak (0: the flat kernel has none, Eq. 3/11),
     # and embedding bytes at HBM bandwidth (read the fp32 input once, write labels)
     job_frames = totals["frames"]
     hbm_bytes = job_frames * (n * d * 4 + n * 4)
     hbm_ms = hbm_bytes / (peaks["hbm_gbs"] * 1e9) * 1e3
-    roof_terms = {"tensor_ms": frame_roof_ms, "sfu_ms": 0.0, "hbm_ms": hbm_ms,
-                  "bound": "tensor" if frame_roof_ms >= hbm_ms else "hbm",
-                  "frac": max(frame_roof_ms, hbm_ms) / ms if ms > 0 else None,
+    roof_terms = {"tensor_ms": job_tensor_ms, "sfu_ms": 0.0, "hbm_ms": hbm_ms,
+                  "bound": "tensor" if job_tensor_ms >= hbm_ms else "hbm",
+                  "frac": max(job_tensor_ms, hbm_ms) / ms if ms > 0 else None,
                   "hbm_peak_gbs": peaks["hbm_gbs"]}
     cb = None
     if world == 1 and not args.no_cpu:

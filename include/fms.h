@@ -86,6 +86,7 @@ typedef struct {
   int64_t iter_seed_iters;    /* sum over K2 launches of active seeds (units of work) */
   int64_t iter_items;         /* sum over K2 launches of work items */
   int64_t launches;           /* kernels this library launched during the call */
+  int64_t iter_count_units;   /* sum over K2 launches of converged modes counted (intensity pass, R10) */
 } fms_run_stats;
 
 fms_status fms_default_policy(fms_seed_policy* out);

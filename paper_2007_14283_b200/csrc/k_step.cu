@@ -57,10 +57,13 @@ __global__ void plan_kernel(Params p) {
     p.counters[0] = s_tiles_total * p.n_chunks;
     p.counters[1] = s_tiles_total;
     p.counters[3] = 0;
-    long long units = 0;
-    for (int f = 0; f < p.B; ++f)
+    long long units = 0, count_units = 0;
+    for (int f = 0; f < p.B; ++f) {
       if (p.ctl[f].n_tiles_step && p.ctl[f].phase == PH_ITERATE) units += p.ctl[f].n_active;
+      if (p.ctl[f].n_tiles_step && p.ctl[f].phase == PH_COUNT) count_units += p.ctl[f].n_active;
+    }
     reinterpret_cast<long long*>(p.counters + 6)[0] = units;  // active seeds this step (A_t summed)
+    reinterpret_cast<long long*>(p.counters + 10)[0] = count_units;  // converged modes counted (R10)
   }
 }
 

@@ -55,6 +55,7 @@ namespace {
 constexpr int kPoll = 4;            // default lockstep steps launched between host polls
 constexpr int kMaxPcap = 8192;      // merge pool capacity (SMEM bitonic sort)
 constexpr int kCounters = 64;
+constexpr int kProfInts = 12;       // counters snapshot per profiled K2 launch
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -78,7 +79,7 @@ struct Ctx {
   size_t h_ctl_cap = 0;
   // profiling
   std::vector<cudaEvent_t> ev;
-  int* h_prof = nullptr;   // per launch: counters[0..7] snapshot
+  int* h_prof = nullptr;   // per launch: counters[0..kProfInts) snapshot
   size_t h_prof_cap = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -375,10 +376,10 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
           if (c->h_prof_cap < slot + 1) {
             size_t ncap = std::max<size_t>(256, 2 * (slot + 1));
             int* np = nullptr;
-            CU(cudaMallocHost(&np, ncap * 8 * sizeof(int)));
+            CU(cudaMallocHost(&np, ncap * kProfInts * sizeof(int)));
             if (c->h_prof) {
               CU(cudaStreamSynchronize(st));
-              memcpy(np, c->h_prof, c->h_prof_cap * 8 * sizeof(int));
+              memcpy(np, c->h_prof, c->h_prof_cap * kProfInts * sizeof(int));
               cudaFreeHost(c->h_prof);
             }
             c->h_prof = np;
@@ -387,7 +388,8 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
           CU(cudaEventRecord(c->ev[2 * slot], st));
           CU(launch_iter(p.DP, tm, p, c->num_sms, st));
           CU(cudaEventRecord(c->ev[2 * slot + 1], st));
-          CU(cudaMemcpyAsync(c->h_prof + slot * 8, p.counters, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+          CU(cudaMemcpyAsync(c->h_prof + slot * kProfInts, p.counters, kProfInts * sizeof(int), cudaMemcpyDeviceToHost,
+                             st));
           ++launches;
         } else {
           CU(launch_iter(p.DP, tm, p, c->num_sms, st));
@@ -497,7 +499,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
     rs->launches = kernels;
     if (c->profile) {
       for (int l = 0; l < launches; ++l) {
-        const int* snap = c->h_prof + (size_t)l * 8;
+        const int* snap = c->h_prof + (size_t)l * kProfInts;
         if (snap[0] <= 0) continue;
         float t = 0.f;
         cudaEventElapsedTime(&t, c->ev[2 * l], c->ev[2 * l + 1]);
@@ -505,6 +507,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
         rs->iter_launches += 1;
         rs->iter_items += snap[0];
         rs->iter_seed_iters += reinterpret_cast<const long long*>(snap + 6)[0];
+        rs->iter_count_units += reinterpret_cast<const long long*>(snap + 10)[0];
       }
     }
   }
