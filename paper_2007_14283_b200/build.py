@@ -35,6 +35,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-o", SO + ".tmp"] + sources()
     if verbose:
         cmd += ["-Xptxas", "-v"]
+    cmd += os.environ.get("FMS_NVCC_EXTRA", "").split()  # timing experiments only (e.g. -DFMS_WAIT_HINT)
     subprocess.check_call(cmd)
     os.replace(SO + ".tmp", SO)
     return SO

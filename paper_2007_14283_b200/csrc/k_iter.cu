@@ -108,6 +108,14 @@ __device__ __forceinline__ void role_wait(uint64_t* bar, uint32_t parity) { mbar
 #else
 __device__ __forceinline__ void role_wait(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
 #endif
+// the epilogue's wait for a similarity tile (timing experiment: -DK2_EPI_SLEEP=ns backs off)
+#ifdef K2_EPI_SLEEP
+__device__ __forceinline__ void epi_wait(uint64_t* bar, uint32_t parity) {
+  if (!mbar_test(bar, parity)) mbar_wait_sleep(bar, parity, K2_EPI_SLEEP);
+}
+#else
+__device__ __forceinline__ void epi_wait(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
+#endif
 
 struct ItemDesc {
   int f, tile, chunk, mode;
@@ -356,7 +364,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         if ((int)(ctile & 1) != grp) continue;
         const int lrole = h ? 15 : 3 + grp * 4 + q;  // timeline: the h == 0 warps
         tlog(p, lrole, ctile, 0);
-        mbar_wait(&c_full[grp], mine & 1);
+        epi_wait(&c_full[grp], mine & 1);
         tlog(p, lrole, ctile, 1);
         const uint32_t pb = ctile % Cfg::NP;
         tc_fence_after();
