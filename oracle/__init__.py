@@ -38,7 +38,10 @@ class Policy(C.Structure):
                 ("L", C.c_double), ("H", C.c_double), ("P", C.c_double),
                 ("has_background", C.c_int32), ("min_instance_px", C.c_int32),
                 ("saturation_stop", C.c_int32), ("max_rounds", C.c_int32),
-                ("rng_seed", C.c_uint64)]
+                ("rng_seed", C.c_uint64), ("profile", C.c_int32), ("pad", C.c_int32)]
+
+
+PROFILE_FLAT, PROFILE_GAUSS = 0, 1
 
 
 class Trace(C.Structure):
@@ -86,6 +89,11 @@ def lib():
                                     C.c_double, C.c_double, C.c_int64, P(np.float64, flags="C"),
                                     P(np.uint8, flags="C"), P(np.int64, flags="C"), P(np.int32, flags="C"),
                                     C.POINTER(C.c_int64)]
+        L.fmso_lockstep_p.restype = C.c_int32
+        L.fmso_lockstep_p.argtypes = L.fmso_lockstep.argtypes + [C.c_int32]
+        L.fmso_window_gauss.restype = C.c_double
+        L.fmso_window_gauss.argtypes = [P(np.float64, flags="C"), C.c_int64, C.c_int32, C.c_double,
+                                        P(np.float64, flags="C"), P(np.float64, flags="C")]
         L.fmso_merge.restype = C.c_int64
         L.fmso_merge.argtypes = [P(np.float64, flags="C"), P(np.int64, flags="C"), P(np.int64, flags="C"),
                                  C.c_int64, C.c_int32, C.c_double, P(np.int64, flags="C")]
@@ -104,9 +112,9 @@ def lib():
 
 
 def policy(kind=SEEDS_OSOP, n_seeds=128, gamma=0.9, L=2.0, H=8.0, P=0.99, has_background=1,
-           min_instance_px=0, saturation_stop=0, max_rounds=8, rng_seed=0) -> Policy:
+           min_instance_px=0, saturation_stop=0, max_rounds=8, rng_seed=0, profile=PROFILE_FLAT) -> Policy:
     return Policy(kind, n_seeds, gamma, L, H, P, has_background, min_instance_px, saturation_stop,
-                  max_rounds, rng_seed)
+                  max_rounds, rng_seed, profile, 0)
 
 
 @dataclass
@@ -166,8 +174,15 @@ def window(xhat: np.ndarray, s: np.ndarray, h: float):
     return g, int(cnt)
 
 
+def window_gauss(xhat: np.ndarray, s: np.ndarray, h: float):
+    g = np.zeros(xhat.shape[1], dtype=np.float64)
+    mass = lib().fmso_window_gauss(np.ascontiguousarray(xhat), xhat.shape[0], xhat.shape[1], h,
+                                   np.ascontiguousarray(s, dtype=np.float64), g)
+    return g, float(mass)
+
+
 def lockstep(xhat: np.ndarray, seeds: np.ndarray, h: float, max_iter: int = 300, tol: float | None = None,
-             gamma: float = 0.9):
+             gamma: float = 0.9, profile: int = PROFILE_FLAT):
     xhat = np.ascontiguousarray(xhat, dtype=np.float64)
     s = np.ascontiguousarray(seeds, dtype=np.float64).copy()
     K = s.shape[0]
@@ -176,8 +191,8 @@ def lockstep(xhat: np.ndarray, seeds: np.ndarray, h: float, max_iter: int = 300,
     its = np.zeros(K, dtype=np.int32)
     sit = C.c_int64(0)
     tol = h / 1000.0 if tol is None else tol
-    t = lib().fmso_lockstep(xhat, xhat.shape[0], xhat.shape[1], h, max_iter, tol, gamma, K, s, st, inten,
-                            its, C.byref(sit))
+    t = lib().fmso_lockstep_p(xhat, xhat.shape[0], xhat.shape[1], h, max_iter, tol, gamma, K, s, st, inten,
+                              its, C.byref(sit), profile)
     return dict(iters=int(t), seeds=s, status=st, intensity=inten, seed_iters_each=its, seed_iters=sit.value)
 
 

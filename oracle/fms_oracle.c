@@ -161,6 +161,26 @@ int64_t fmso_window(const double* xhat, int64_t n, int32_t d, double tau, const 
 }
 
 /* ---------------------------------------------------------------------------------------------
+ * NEXT-4, reading R23: Eq. 2 admits any profile k; the Gaussian profile
+ * k(t) = exp(-t/2) with t = |x - s|^2 / h, and |x - s|^2 = 2 (1 - x.s) for unit vectors (Eq. 9), gives
+ *     w_i = exp(-(1 - x_i.s) / h),   g(s) = sum_i w_i x_i   (ascending i; every point contributes)
+ * and the mean-shift vector (Eq. 5-6 with g = -k' proportional to k) is g / sum_i w_i.
+ * ------------------------------------------------------------------------------------------- */
+double fmso_window_gauss(const double* xhat, int64_t n, int32_t d, double h, const double* s, double* g) {
+  double wsum = 0.0;
+  for (int32_t k = 0; k < d; ++k) g[k] = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double* x = xhat + i * d;
+    double dot = 0.0;
+    for (int32_t k = 0; k < d; ++k) dot += x[k] * s[k];
+    const double w = exp(-(1.0 - dot) / h);
+    for (int32_t k = 0; k < d; ++k) g[k] += w * x[k];
+    wsum += w;
+  }
+  return wsum;
+}
+
+/* ---------------------------------------------------------------------------------------------
  * Alg. 2 lines 4-9 with the convergence rule of P:223 and early stopping:
  * all active seeds advance once per lockstep iteration (the batched-tensor form of P:210):
  *     s' = m_h(s)/|m_h(s)| = g/|g|              (R4: renormalised onto the unit sphere)
@@ -173,6 +193,14 @@ int64_t fmso_window(const double* xhat, int64_t n, int32_t d, double tau, const 
 int32_t fmso_lockstep(const double* xhat, int64_t n, int32_t d, double h, int32_t max_iter,
                       double tol, double gamma, int64_t K, double* seeds, uint8_t* status,
                       int64_t* intensity, int32_t* iters, int64_t* seed_iters) {
+  return fmso_lockstep_p(xhat, n, d, h, max_iter, tol, gamma, K, seeds, status, intensity, iters, seed_iters,
+                         FMSO_PROFILE_FLAT);
+}
+
+/* the same with the profile of the update selectable (flat: the paper; Gaussian: NEXT-4, R23) */
+int32_t fmso_lockstep_p(const double* xhat, int64_t n, int32_t d, double h, int32_t max_iter,
+                        double tol, double gamma, int64_t K, double* seeds, uint8_t* status,
+                        int64_t* intensity, int32_t* iters, int64_t* seed_iters, int32_t profile) {
   const double tau = 1.0 - h;
   const int32_t need = fmso_need(gamma, K);
   int32_t t_run = 0;
@@ -189,8 +217,9 @@ int32_t fmso_lockstep(const double* xhat, int64_t n, int32_t d, double h, int32_
       if (status[j] != 0) continue;
       double g[256], sn[256];
       double* s = seeds + j * d;
-      int64_t cnt = fmso_window(xhat, n, d, tau, s, g);
-      if (cnt == 0) { status[j] = 2; continue; }
+      const double mass = profile == FMSO_PROFILE_GAUSS ? fmso_window_gauss(xhat, n, d, h, s, g)
+                                                         : (double)fmso_window(xhat, n, d, tau, s, g);
+      if (mass == 0.0) { status[j] = 2; continue; }
       double nn = 0.0;
       for (int32_t k = 0; k < d; ++k) nn += g[k] * g[k];
       nn = sqrt(nn);
@@ -302,6 +331,7 @@ int fmso_cluster(const float* emb, int64_t n, int32_t d, double h, int32_t max_i
   if (!(pol->gamma > 0.0 && pol->gamma <= 1.0)) return FMSO_E_INVALID;
   if (pol->kind == FMSO_SEEDS_OSOP && (!(pol->P > 0.0 && pol->P < 1.0) || !(pol->L > 0.0)))
     return FMSO_E_INVALID;
+  if (pol->profile != FMSO_PROFILE_FLAT && pol->profile != FMSO_PROFILE_GAUSS) return FMSO_E_INVALID;
 
   const double tau = 1.0 - h;
   const double rho = h;
@@ -343,7 +373,8 @@ int fmso_cluster(const float* emb, int64_t n, int32_t d, double h, int32_t max_i
     for (int64_t j = 0; j < Kr; ++j) memcpy(seeds + j * d, xhat + idx[j] * d, (size_t)d * sizeof(double));
     double gam = pol->kind == FMSO_SEEDS_ALL ? 1.0 : pol->gamma;
     int64_t sit = 0;
-    int32_t t_run = fmso_lockstep(xhat, n, d, h, max_iter, tol, gam, Kr, seeds, st, inten, its, &sit);
+    int32_t t_run = fmso_lockstep_p(xhat, n, d, h, max_iter, tol, gam, Kr, seeds, st, inten, its, &sit,
+                                    pol->profile);
 
     int64_t nconv = 0, ndisc = 0;
     for (int64_t j = 0; j < Kr; ++j) { nconv += st[j] == 1; ndisc += st[j] != 1; }

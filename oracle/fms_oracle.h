@@ -31,7 +31,11 @@ typedef struct {
   int32_t saturation_stop; /* stop when a round adds no counted instance (R22) */
   int32_t max_rounds;      /* <= FMSO_MAX_ROUNDS */
   uint64_t rng_seed;       /* hash-priority selection salt (R11) */
+  int32_t profile;         /* kernel profile of the iteration: FMSO_PROFILE_FLAT (Eq. 3/11, the paper) or
+                              FMSO_PROFILE_GAUSS (NEXT-4, reading R23) */
+  int32_t pad;
 } fmso_policy;
+enum { FMSO_PROFILE_FLAT = 0, FMSO_PROFILE_GAUSS = 1 };
 
 typedef struct {
   int32_t rounds, K;
@@ -65,6 +69,15 @@ int64_t fmso_select(const uint8_t* cand, int64_t n, int64_t K, uint64_t rng_seed
                     int32_t round, int64_t* out);                                 /* Alg. 2 l.2 */
 int64_t fmso_window(const double* xhat, int64_t n, int32_t d, double tau,
                     const double* s, double* g);                                  /* Eq. 8+11 */
+/* NEXT-4, reading R23: the Gaussian profile of Eq. 2, k(t) = exp(-t/2) at
+ * t = |x - s|^2 / h = 2 (1 - x.s) / h for unit vectors: every point weighs w = exp(-(1 - x.s)/h).
+ * g = sum_i w_i x_i (ascending i); returns sum_i w_i. */
+double fmso_window_gauss(const double* xhat, int64_t n, int32_t d, double h, const double* s, double* g);
+/* fmso_lockstep with the kernel profile of the update selectable (FMSO_PROFILE_*); the intensity
+ * stays the flat window count |S_h(m)| (R10) for both profiles. */
+int32_t fmso_lockstep_p(const double* xhat, int64_t n, int32_t d, double h, int32_t max_iter,
+                        double tol, double gamma, int64_t K, double* seeds, uint8_t* status,
+                        int64_t* intensity, int32_t* iters, int64_t* seed_iters, int32_t profile);
 /* Lockstep mean-shift over K seeds (Alg. 2 l.4-9 + early stop).  seeds[K*d] in/out, status[K]:
  * 1 converged, 2 stalled, 3 discarded.  Returns iterations run; writes, for converged seeds, the
  * intensity |S_h(m)| (flat-kernel density of Eq. 2 at the mode, R10) and per-seed iterations. */
