@@ -43,6 +43,9 @@ def parse():
                     help="replicas: every rank clusters its own frames (weak scaling); seeds: every rank "
                          "clusters the same frames and iterates 1/N of each round's seeds (strong scaling, "
                          "SURVEY 8(e)2; exchange through torch.distributed)")
+    ap.add_argument("--kernel-profile", default="flat", choices=["flat", "gauss"],
+                    help="kernel of the mean-shift update: the paper's flat kernel, or the Gaussian profile "
+                         "(NEXT-4, reading R23; SFU-bound)")
     ap.add_argument("--no-seed-shard", action="store_true",
                     help="with N > 1 replicas: skip the extra seed-sharded C4 measurement")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
@@ -308,6 +311,9 @@ def main():
     if sharded:
         from paper_2007_14283_b200.dist import enable_seed_sharding
         enable_seed_sharding(ctx)
+    gauss = args.kernel_profile == "gauss"
+    if gauss:
+        ctx.set_option("kernel_profile", 1)
     pol = fms.default_policy(**policy_kwargs(n))
     stream = torch.cuda.current_stream(dev)
 
@@ -407,6 +413,25 @@ def main():
                   "bound": "tensor" if job_tensor_ms >= hbm_ms else "hbm",
                   "frac": max(job_tensor_ms, hbm_ms) / ms if ms > 0 else None,
                   "hbm_peak_gbs": peaks["hbm_gbs"]}
+    # SFU term: the Gaussian profile evaluates one exp2 (MUFU.EX2) per (active seed, pixel) pair of
+    # the iteration steps; peak = 148 SMs x 16 MUFU results/clk/SM x the max SM clock (DESIGN 6)
+    clk_ghz = (peaks.get("sm_max_mhz") or 1965.0) / 1e3
+    sfu_peak = 148 * 16 * clk_ghz  # G exp2/s
+    exps = totals["iter_seed_iters"] * n if gauss else 0
+    sfu_ms = exps / (sfu_peak * 1e9) * 1e3
+    if gauss:
+        roof_terms["sfu_ms"] = sfu_ms
+        roof_terms["sfu_peak_gexp2_s"] = sfu_peak
+        if sfu_ms > max(job_tensor_ms, hbm_ms):
+            roof_terms["bound"] = "sfu"
+            roof_terms["frac"] = sfu_ms / ms if ms > 0 else None
+        ach = exps / (totals["iter_ms"] / 1e3) / 1e9 if totals["iter_ms"] > 0 else None
+        roof = {"bound": "sfu", "kernel": "fms::iter_kernel<16, true> (K2, Gaussian profile)", "achieved": ach,
+                "peak": sfu_peak, "unit": "Gexp2/s", "frac": (ach / sfu_peak) if ach else None, "traffic": None,
+                "peak_source": "derived: 148 SMs x 16 MUFU.EX2/clk/SM x sm_max_mhz",
+                "tensor_achieved_tflops": achieved, "tensor_peak_tflops": peak,
+                "ms_per_launch": totals["iter_ms"] / max(1, totals["iter_launches"]),
+                "iter_share_of_step": totals["iter_ms"] / ms if ms > 0 else None}
     cb = None
     if world == 1 and not args.no_cpu:
         cb = cpu_baseline([synth.make_frame(args.config, 20000 + i) for i in range(3)], budget_s=20.0)
@@ -418,7 +443,8 @@ def main():
         "vs_baseline": None,
         "dtype": "f16x3 split / f32 accumulate", "data": "synthetic",
         "config": {"workload": f"{args.config}: {f0.H}x{f0.W} frame, {d}-D, {f0.cells} touching/overlapping cells "
-                               f"+ background, full OSOP (N_initial 128, gamma 0.9, L 2, P 0.99)",
+                               f"+ background, full OSOP (N_initial 128, gamma 0.9, L 2, P 0.99)"
+                               + (", Gaussian kernel profile (NEXT-4)" if gauss else ""),
                    "frames_per_step": B, "l2": "2 alternating input batches of B x 16 MiB (> 126 MB L2)",
                    "parallelism": f"seed-sharded x{world} ({args.backend})" if sharded else f"replicas x{world}"},
         "roofline": roof,

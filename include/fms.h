@@ -151,7 +151,13 @@ fms_status fms_set_pixel_shard(void* ctx, fms_exchange_fn fn, void* user, int32_
 
 /* Options: "profile_iter" (0/1): time every K2 launch with CUDA events for fms_run_stats.iter_ms.
  *          "poll_steps" (1..64, default 4): lockstep steps launched between two host polls of the
- *          device counters (a frame that finishes early idles at most poll_steps - 1 steps). */
+ *          device counters (a frame that finishes early idles at most poll_steps - 1 steps).
+ *          "kernel_profile" (0/1, default 0): the kernel of the mean-shift update.  0 = the paper's
+ *          flat kernel (Eq. 3 / Eq. 11).  1 = Gaussian profile (SURVEY NEXT-4,
+ *          DESIGN reading R23): Eq. 2's k(t) = exp(-t/2) at t = |x - s|^2 / h, i.e. every pixel
+ *          weighs w = exp(-(1 - x.s)/h) in s' = normalize(sum_i w_i x_i) (fp16 weights; weights
+ *          below 2^-24 flush to zero).  Intensity, merge, coverage and assignment keep the flat
+ *          window in both.  Pixel sharding requires 0 (FMS_E_INVALID at the clustering call). */
 fms_status fms_set_option(void* ctx, const char* key, int64_t value);
 
 /* Cluster one frame.  emb: device, [n][d] fp32 row-major.  labels: device int32[n] in [0, K).

@@ -86,6 +86,20 @@ __device__ __forceinline__ uint32_t flat_kernel_pair(float c0, float c1, float k
 }
 constexpr double kPScale = 1.0 / 131072.0;  // value of an in-window weight, 2^-17
 
+// NEXT-4, reading R23: Gaussian profile of Eq. 2 on unit vectors, w = exp(-(1 - c)/h) =
+// exp2(C ka + kb) with C = 2^11 c, ka = log2(e) / (2^11 h), kb = -log2(e) / h: one FFMA and one
+// MUFU.EX2 per pixel, and one F2FP packs a pair of weights into fp16 (low half = first pixel).
+// Weights below the fp16 range (< 2^-24, i.e. 1 - c > 16.6 h) flush to zero.  The weighted sums are
+// no longer exact (fp16 weights, ~2^-11 relative), so results match the fp64 oracle to a tolerance.
+__device__ __forceinline__ uint32_t gauss_pair(float c0, float c1, float ka, float kb) {
+  float w0, w1;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(w0) : "f"(__fmaf_rn(c0, ka, kb)));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(w1) : "f"(__fmaf_rn(c1, ka, kb)));
+  uint32_t m;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(m) : "f"(w1), "f"(w0));  // a -> upper half, b -> lower
+  return m;
+}
+
 // Timing experiments (tools/iter_probe.cu): -DFMS_K2_VARIANT=bits switches parts of the kernel off
 // (1 weighted-sum MMAs, 2 weight stores, 8/12 similarity MMAs, 16 C loads, 64 pixel loads), -DFMS_K2_TIMELINE logs a clock64 timeline of CTA 0.  The production
 // build compiles both hooks away.
@@ -126,7 +140,7 @@ __device__ __forceinline__ ItemDesc item_desc(const Params& p, int item) {
   return ItemDesc{tt.f, tt.tile, item - t * p.n_chunks, tt.mode};
 }
 
-template <int DP>
+template <int DP, bool GAUSS>
 __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_constant__ TMaps tm, Params p) {
   using Cfg = IterCfg<DP>;
   const int n_items = p.counters[0];
@@ -312,6 +326,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     // C is scaled by 2^11 (exact); k_tau = -8192 tau_m, tau_m = the float just below 2^11 tau
     const float k_tau = -8192.0f * __uint_as_float(__float_as_uint(p.tau_f * kLimb) - 1u);
+    const float g_ka = GAUSS ? (float)(1.4426950408889634 / (p.h * (double)kLimb)) : 0.f;  // Gaussian (R23)
+    const float g_kb = GAUSS ? (float)(-1.4426950408889634 / p.h) : 0.f;
     const uint32_t cbase = tmem + lane_base + grp * kBN + h * kColsPerWarp;
     uint32_t ctile = 0;                               // running tile index over the CTA's stream
     uint32_t mine = 0;                                // tiles handled by this group so far
@@ -351,7 +367,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
 #pragma unroll
         for (int k = 0; k < DP; ++k) {
           // exact sums of multiples of 2^-28 in fp64; dividing by the power of two 2^-17 is exact
-          if (gs[k * kBM] != 0.0) atomicAdd(dst + k, gs[k * kBM] / kPScale);
+          if (gs[k * kBM] != 0.0) atomicAdd(dst + k, GAUSS ? gs[k * kBM] : gs[k * kBM] / kPScale);
           gs[k * kBM] = 0.0;
         }
       }
@@ -384,9 +400,15 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         const bool need_free = w.mode == 0 && ctile >= (uint32_t)Cfg::NP;
         bool p_free = !need_free || mbar_test(&x_empty[u % Cfg::STAGES], (u / Cfg::STAGES) & 1);
         uint32_t pk[kColsPerWarp / 2];
+        if (GAUSS && w.mode == 0) {  // count passes (intensity, R10) keep the flat window
 #pragma unroll
-        for (int i = 0; i < kColsPerWarp / 2; ++i)
-          pk[i] = flat_kernel_pair(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]), k_tau);
+          for (int i = 0; i < kColsPerWarp / 2; ++i)
+            pk[i] = gauss_pair(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]), g_ka, g_kb);
+        } else {
+#pragma unroll
+          for (int i = 0; i < kColsPerWarp / 2; ++i)
+            pk[i] = flat_kernel_pair(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]), k_tau);
+        }
         tlog(p, lrole, ctile, 5);
         if (!p_free) mbar_wait(&x_empty[u % Cfg::STAGES], (u / Cfg::STAGES) & 1);
         tlog(p, lrole, ctile, 6);
@@ -432,18 +454,24 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
 int iter_smem_bytes(int DP) { return DP == 16 ? IterCfg<16>::SMEM : IterCfg<32>::SMEM; }
 
 cudaError_t launch_iter(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st) {
+  const bool g = p.profile == 1;
   if (DP == 16) {
-    iter_kernel<16><<<grid, kIterThreads, IterCfg<16>::SMEM, st>>>(tm, p);
+    if (g) iter_kernel<16, true><<<grid, kIterThreads, IterCfg<16>::SMEM, st>>>(tm, p);
+    else iter_kernel<16, false><<<grid, kIterThreads, IterCfg<16>::SMEM, st>>>(tm, p);
   } else {
-    iter_kernel<32><<<grid, kIterThreads, IterCfg<32>::SMEM, st>>>(tm, p);
+    if (g) iter_kernel<32, true><<<grid, kIterThreads, IterCfg<32>::SMEM, st>>>(tm, p);
+    else iter_kernel<32, false><<<grid, kIterThreads, IterCfg<32>::SMEM, st>>>(tm, p);
   }
   return cudaGetLastError();
 }
 
 cudaError_t setup_iter_attrs() {
-  cudaError_t e = cudaFuncSetAttribute(iter_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, IterCfg<16>::SMEM);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(iter_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, IterCfg<32>::SMEM);
+  const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  cudaError_t e = cudaFuncSetAttribute(iter_kernel<16, false>, a, IterCfg<16>::SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(iter_kernel<16, true>, a, IterCfg<16>::SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(iter_kernel<32, false>, a, IterCfg<32>::SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(iter_kernel<32, true>, a, IterCfg<32>::SMEM);
+  return e;
 }
 
 }  // namespace fms

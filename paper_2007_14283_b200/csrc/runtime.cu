@@ -95,6 +95,7 @@ struct Ctx {
   void* pbuf = nullptr;  // exchange buffer, grown on demand
   size_t pbuf_bytes = 0;
   int poll = kPoll;  // lockstep steps between host polls ("poll_steps")
+  int kprofile = 0;  // "kernel_profile": 0 flat (the paper), 1 Gaussian (NEXT-4)
 };
 
 fms_status fail(Ctx* c, fms_status s, const std::string& m) {
@@ -225,6 +226,9 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   const bool pshard = c->pworld > 1;
   if (pshard && (c->poff < 0 || c->poff + n > c->pn_glob))
     return fail(c, FMS_E_INVALID, "pixel shard [offset, offset + n) outside the frame of n_global pixels");
+  if (pshard && c->kprofile != 0)
+    return fail(c, FMS_E_INVALID, "pixel sharding needs the flat kernel (its window sums are exchanged exactly)");
+  p.profile = c->kprofile;
   p.n_glob = pshard ? c->pn_glob : n;
   p.pix_off = pshard ? c->poff : 0;
   p.pworld = pshard ? c->pworld : 1;
@@ -619,6 +623,11 @@ fms_status fms_set_option(void* ctx, const char* key, int64_t value) {
   if (!c || !key) return FMS_E_INVALID;
   if (!strcmp(key, "profile_iter")) {
     c->profile = value != 0;
+    return FMS_OK;
+  }
+  if (!strcmp(key, "kernel_profile")) {
+    if (value < 0 || value > 1) return fail(c, FMS_E_INVALID, "kernel_profile must be 0 (flat) or 1 (Gaussian)");
+    c->kprofile = (int)value;
     return FMS_OK;
   }
   if (!strcmp(key, "poll_steps")) {  // a frame that finishes idles at most poll_steps - 1 steps
