@@ -177,7 +177,11 @@ fms_status fms_cluster_batch(void* ctx, const float* emb, int32_t B, int64_t n, 
                              fms_run_stats* run_stats, void* stream);
 
 /* Same as fms_cluster_batch with HOST buffers: the embeddings are copied to the device, and labels /
- * centres copied back, inside the call (end-to-end entry).  Pinned host memory is recommended. */
+ * centres copied back, inside the call (end-to-end entry).  The batch runs in chunks of option
+ * "host_chunk" frames (default 32) through double-buffered device staging: a copy stream uploads
+ * chunk i+1 and downloads chunk i-1's results while chunk i is clustered (frames are independent, so
+ * the results equal one fms_cluster_batch over all B frames).  Pinned host memory is needed for the
+ * copies to overlap.  run_stats sums the chunks' counters. */
 fms_status fms_cluster_batch_host(void* ctx, const float* emb_host, int32_t B, int64_t n, int32_t d,
                                   double bandwidth, int32_t max_iters, double tol,
                                   const fms_seed_policy* policy, int32_t* labels_host, float* centres_host,

@@ -96,6 +96,10 @@ struct Ctx {
   size_t pbuf_bytes = 0;
   int poll = kPoll;  // lockstep steps between host polls ("poll_steps")
   int kprofile = 0;  // "kernel_profile": 0 flat (the paper), 1 Gaussian (NEXT-4)
+  // host-buffer entry: chunked, double-buffered staging on a copy stream ("host_chunk")
+  int host_chunk = 32;
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr}, ev_done = nullptr;
 };
 
 fms_status fail(Ctx* c, fms_status s, const std::string& m) {
@@ -315,6 +319,12 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
     if (bytes > c->pbuf_bytes) {
       CU(cudaStreamSynchronize(st));
       if (c->pbuf) cudaFree(c->pbuf);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
+    if (c->ev_out[i]) cudaEventDestroy(c->ev_out[i]);
+  }
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
+  if (c->cstream) cudaStreamDestroy(c->cstream);
       c->pbuf = nullptr;
       c->pbuf_bytes = 0;
       if (cudaMalloc(&c->pbuf, bytes) != cudaSuccess) {
@@ -566,6 +576,12 @@ void fms_ctx_destroy(void* ctx) {
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->h_prof) cudaFreeHost(c->h_prof);
   if (c->pbuf) cudaFree(c->pbuf);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
+    if (c->ev_out[i]) cudaEventDestroy(c->ev_out[i]);
+  }
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
+  if (c->cstream) cudaStreamDestroy(c->cstream);
   for (auto e : c->ev) cudaEventDestroy(e);
   if (c->t0) cudaEventDestroy(c->t0);
   if (c->t1) cudaEventDestroy(c->t1);
@@ -623,6 +639,11 @@ fms_status fms_set_option(void* ctx, const char* key, int64_t value) {
   if (!c || !key) return FMS_E_INVALID;
   if (!strcmp(key, "profile_iter")) {
     c->profile = value != 0;
+    return FMS_OK;
+  }
+  if (!strcmp(key, "host_chunk")) {  // frames per chunk of fms_cluster_batch_host
+    if (value < 1 || value > 1 << 20) return fail(c, FMS_E_INVALID, "host_chunk must be >= 1");
+    c->host_chunk = (int)value;
     return FMS_OK;
   }
   if (!strcmp(key, "kernel_profile")) {
@@ -715,31 +736,90 @@ fms_status fms_cluster_batch_host(void* ctx, const float* emb_host, int32_t B, i
     return fail(c, FMS_E_INVALID, "null buffer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CU(cudaSetDevice(c->device));
-  const size_t eb = align_up((size_t)B * n * d * 4, 1024);
-  const size_t lb = align_up((size_t)B * n * 4, 1024);
-  const size_t cb = align_up((size_t)B * std::max(centres_cap, 1) * d * 4, 1024);
-  if (eb + lb + cb > c->stage_bytes) {
+  // The batch runs in chunks of up to host_chunk frames with double-buffered staging: the copy
+  // stream uploads chunk i+1 (and downloads chunk i-1's results) while chunk i is clustered, so the
+  // PCIe transfers overlap the compute (frames are independent, so chunking changes no result).
+  const int32_t chunk = std::max(1, std::min<int32_t>(B, c->host_chunk));
+  const int nchunks = (B + chunk - 1) / chunk;
+  const int nbuf = nchunks > 1 ? 2 : 1;
+  const size_t eb = align_up((size_t)chunk * n * d * 4, 1024);
+  const size_t lb = align_up((size_t)chunk * n * 4, 1024);
+  const size_t cb = align_up((size_t)chunk * std::max(centres_cap, 1) * d * 4, 1024);
+  const size_t per = eb + lb + cb;
+  if (per * nbuf > c->stage_bytes) {
     if (c->stage) cudaFree(c->stage);
     c->stage = nullptr;
     c->stage_bytes = 0;
-    if (cudaMalloc(&c->stage, eb + lb + cb) != cudaSuccess) {
+    if (cudaMalloc(&c->stage, per * nbuf) != cudaSuccess) {
       cudaGetLastError();
       return fail(c, FMS_E_OOM, "staging allocation failed");
     }
-    c->stage_bytes = eb + lb + cb;
+    c->stage_bytes = per * nbuf;
   }
-  float* d_emb = reinterpret_cast<float*>(c->stage);
-  int32_t* d_lab = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(c->stage) + eb);
-  float* d_cen = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(c->stage) + eb + lb);
-  CU(cudaMemcpyAsync(d_emb, emb_host, (size_t)B * n * d * 4, cudaMemcpyHostToDevice, st));
-  fms_status s = run_batch(c, d_emb, B, n, d, bandwidth, max_iters, tol, policy, d_lab, d_cen, centres_cap, K_out,
-                           frame_stats, run_stats, st);
-  if (s != FMS_OK && s != FMS_E_CAPACITY) return s;
-  CU(cudaMemcpyAsync(labels_host, d_lab, (size_t)B * n * 4, cudaMemcpyDeviceToHost, st));
-  if (centres_cap > 0)
-    CU(cudaMemcpyAsync(centres_host, d_cen, (size_t)B * centres_cap * d * 4, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  return s;
+  if (!c->cstream) {
+    CU(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CU(cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming));
+    }
+    CU(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+  }
+  cudaStream_t cs = c->cstream;
+  auto buf = [&](int i) { return reinterpret_cast<uint8_t*>(c->stage) + (size_t)(i % nbuf) * per; };
+  auto rows = [&](int i) { return std::min<int32_t>(chunk, B - i * chunk); };
+  auto h2d = [&](int i) -> cudaError_t {
+    const cudaError_t e = cudaMemcpyAsync(buf(i), emb_host + (size_t)i * chunk * n * d, (size_t)rows(i) * n * d * 4,
+                                          cudaMemcpyHostToDevice, cs);
+    return e != cudaSuccess ? e : cudaEventRecord(c->ev_in[i % nbuf], cs);
+  };
+  // the stream the caller passed must see earlier work on it before the copies start
+  CU(cudaEventRecord(c->ev_done, st));
+  CU(cudaStreamWaitEvent(cs, c->ev_done, 0));
+  CU(h2d(0));
+  fms_status result = FMS_OK;
+  fms_run_stats acc{};
+  for (int i = 0; i < nchunks; ++i) {
+    if (i + 1 < nchunks) {
+      if (i >= 1) CU(cudaStreamWaitEvent(cs, c->ev_done, 0));  // chunk i-1 no longer reads buf (i+1) % 2
+      CU(h2d(i + 1));
+    }
+    CU(cudaStreamWaitEvent(st, c->ev_in[i % nbuf], 0));
+    if (i >= nbuf) CU(cudaStreamWaitEvent(st, c->ev_out[i % nbuf], 0));  // results of chunk i-2 downloaded
+    float* d_emb = reinterpret_cast<float*>(buf(i));
+    int32_t* d_lab = reinterpret_cast<int32_t*>(buf(i) + eb);
+    float* d_cen = reinterpret_cast<float*>(buf(i) + eb + lb);
+    const int32_t Bi = rows(i);
+    // rows >= K of the downloaded centres read as zeros (the device writes rows < K only)
+    if (centres_cap > 0) CU(cudaMemsetAsync(d_cen, 0, (size_t)Bi * centres_cap * d * 4, st));
+    fms_run_stats rs{};
+    fms_status s = run_batch(c, d_emb, Bi, n, d, bandwidth, max_iters, tol, policy, d_lab, d_cen, centres_cap,
+                             K_out + (size_t)i * chunk, frame_stats ? frame_stats + (size_t)i * chunk : nullptr,
+                             &rs, st);
+    if (s != FMS_OK && s != FMS_E_CAPACITY) {
+      cudaStreamSynchronize(cs);
+      return s;
+    }
+    if (s != FMS_OK && result == FMS_OK) result = s;
+    acc.ms_total += rs.ms_total;
+    acc.workspace_bytes = std::max(acc.workspace_bytes, rs.workspace_bytes);
+    acc.steps += rs.steps;
+    acc.iter_launches += rs.iter_launches;
+    acc.iter_ms += rs.iter_ms;
+    acc.iter_seed_iters += rs.iter_seed_iters;
+    acc.iter_items += rs.iter_items;
+    acc.launches += rs.launches;
+    acc.iter_count_units += rs.iter_count_units;
+    CU(cudaEventRecord(c->ev_done, st));
+    CU(cudaStreamWaitEvent(cs, c->ev_done, 0));
+    CU(cudaMemcpyAsync(labels_host + (size_t)i * chunk * n, d_lab, (size_t)Bi * n * 4, cudaMemcpyDeviceToHost, cs));
+    if (centres_cap > 0)
+      CU(cudaMemcpyAsync(centres_host + (size_t)i * chunk * centres_cap * d, d_cen, (size_t)Bi * centres_cap * d * 4,
+                         cudaMemcpyDeviceToHost, cs));
+    CU(cudaEventRecord(c->ev_out[i % nbuf], cs));
+  }
+  CU(cudaStreamSynchronize(cs));
+  if (run_stats) *run_stats = acc;
+  return result;
 }
 
 }  // extern "C"

@@ -197,6 +197,25 @@ def test_host_entry_matches_device_entry():
     assert torch.equal(lh, ld.cpu()) and torch.equal(ch, cd.cpu())
 
 
+def test_host_entry_chunked_overlap_matches_device_entry():
+    # 5 frames in chunks of 2 (ragged last chunk): uploads, compute and downloads overlap on two streams
+    import torch
+    fms = _fms()
+    frames = [synth.make_frame("S1", 10 + s) for s in range(5)]
+    X = np.stack([f.emb for f in frames])
+    pol = fms.default_policy(min_instance_px=min_instance_px(frames[0].n), saturation_stop=1)
+    ld, cd, Kd, _ = fms.cluster(torch.from_numpy(X).cuda(), policy=pol, centres_cap=128)
+    ctx = fms.Context(0)
+    ctx.set_option("host_chunk", 2)
+    eh = torch.from_numpy(X).pin_memory()
+    lh = torch.full((5, frames[0].n), -1, dtype=torch.int32).pin_memory()
+    ch = torch.zeros((5, 128, frames[0].D), dtype=torch.float32).pin_memory()
+    for _ in range(2):  # the second call reuses the staging buffers
+        rc, Kh, rs = ctx.cluster_host(eh, lh, ch, 128, policy=pol)
+        assert Kh == Kd
+        assert torch.equal(lh, ld.cpu()) and torch.equal(ch, cd.cpu())
+
+
 # ---------------------------------------------------------------------------------------------
 # edge cases
 # ---------------------------------------------------------------------------------------------
