@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kAsgThreads, 1) assign_tc_kernel(const __grid_
     const int grp = (warp - kAsgEpiWarp0) >> 2;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const float tau2 = p.tau_f * kLimb;  // D is 2^11-scaled
-    int i = 0, last_f = -1, fcount = 0;
+    int fcount = 0;
     int cand = 0;
     auto flush = [&](int f, int hb) {  // per-frame histogram and candidate count -> global
       asm volatile("bar.sync 1, %0;" ::"n"(kAsgEpiThreads) : "memory");  // the epilogue warps
@@ -205,110 +205,74 @@ __global__ void __launch_bounds__(kAsgThreads, 1) assign_tc_kernel(const __grid_
       cand = 0;
       asm volatile("bar.sync 1, %0;" ::"n"(kAsgEpiThreads) : "memory");
     };
-    // Items are walked with an incremental (frame, tile) cursor: a division per item would cost
-    // more than the tile's argmax.
-    struct Cur {
-      int item, f, t;
-    };
-    auto step = [&](Cur& c) {
-      ++c.item;
-      if (++c.t == p.n_ptiles) { c.t = 0; ++c.f; }
-    };
-    int act_f = -1;
-    bool act_v = false;
-    auto active = [&](int f) -> bool {  // frame-active test, cached (frames change rarely)
-      if (f != act_f) { act_f = f; act_v = asg_frame_active(p, f); }
-      return act_v;
-    };
-    auto flag_of = [&](const Cur& c) -> uint8_t {
-      const long long px = (long long)c.t * kBN + q * 32 + lane;
-      return px < p.n ? p.flags[flag_at(p, c.f, px)] : 0;
-    };
-    // this group's next tile: the kAsgGroups-th active item after c
-    auto next_mine = [&](Cur c) -> Cur {
-      for (int k = 0; k < kAsgGroups;) {
-        step(c);
-        if (c.item >= i_end) return c;
-        if (active(c.f)) ++k;
-      }
-      return c;
-    };
-    const Cur c0{i_begin, i_begin / p.n_ptiles, i_begin - (i_begin / p.n_ptiles) * p.n_ptiles};
-    Cur pf = c0;  // first tile of this group: the (grp+1)-th active item
-    for (int k = 0; pf.item < i_end; step(pf)) {
-      if (!active(pf.f)) continue;
-      if (k++ == grp) break;
-    }
-    uint8_t pf_flag = pf.item < i_end ? flag_of(pf) : 0;
-    for (Cur c = c0; c.item < i_end; step(c)) {
-      const int f = c.f, t = c.t;
-      if (!active(f)) continue;
-      if (f != last_f) {
-        if (last_f >= 0) flush(last_f, (fcount - 1) & 1);
-        last_f = f;
-        ++fcount;
-      }
-      const int my = i;
-      ++i;
-      if (my % kAsgGroups != grp) continue;
-      // The pixel flags come from global memory; the read for the group's next tile is issued
-      // now, so its latency overlaps this tile.
-      const uint8_t fl = pf_flag;  // pf == c
-      pf = next_mine(c);
-      if (pf.item < i_end) pf_flag = flag_of(pf);
-      const uint32_t db = my % kAsgGroups;
+    // Walk the CTA's item range frame by frame: a frame is active (assigned here) or not as a whole,
+    // so the active items form contiguous runs and group grp takes every kAsgGroups-th of them
+    // directly (the producer and the MMA warp number the same active items 0, 1, 2, ...).
+    int n_act = 0;  // active items of this CTA before the current frame
+    for (int f = i_begin / p.n_ptiles; (long long)f * p.n_ptiles < i_end; ++f) {
+      const int s0 = max(i_begin, f * p.n_ptiles), s1 = min(i_end, (f + 1) * p.n_ptiles);
+      if (!asg_frame_active(p, f)) continue;
+      ++fcount;
       const int Kc = p.ctl[f].Kc;
-      mbar_wait(&d_full[db], (my / kAsgGroups) & 1);
-      tc_fence_after();
-      // argmax over the row in four interleaved streams (short dependency chains); each stream
-      // keeps its first maximum, the merge prefers the larger value, then the lower index
-      float bv[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-      int bl[4] = {0, 1, 2, 3};
-      const uint32_t dbase = tmem + lane_base + db * kAsgMaxN;
-      for (int c0 = 0; c0 < Kc; c0 += 64) {
-        uint32_t v[64];
-        tmem_ld64(dbase + c0, v);
-        tmem_ld_wait();
-        // only the 16-column groups that hold centres (compile-time bodies: v stays in registers);
-        // columns past Kc in the last group read as -inf
-        const int nk = min(64, Kc - c0);
-        auto scan = [&](auto groups) {
-          constexpr int G16 = decltype(groups)::value;
-#pragma unroll
-          for (int k = 0; k < 16 * G16; ++k) {
-            const float dv = (k < 16 * (G16 - 1) || k < nk) ? __uint_as_float(v[k]) : -INFINITY;
-            if (dv > bv[k & 3]) { bv[k & 3] = dv; bl[k & 3] = c0 + k; }
+      for (int item = s0 + (((grp - n_act) % kAsgGroups) + kAsgGroups) % kAsgGroups; item < s1;
+           item += kAsgGroups) {
+        const int my = n_act + (item - s0);
+        const int t = item - f * p.n_ptiles;
+        const long long px = (long long)t * kBN + q * 32 + lane;
+        const uint8_t fl = px < p.n ? p.flags[flag_at(p, f, px)] : 0;  // latency overlaps the wait below
+        const uint32_t db = my % kAsgGroups;
+        mbar_wait(&d_full[db], (my / kAsgGroups) & 1);
+        tc_fence_after();
+        // argmax over the row in four interleaved streams (short dependency chains); each stream
+        // keeps its first maximum, the merge prefers the larger value, then the lower index
+        float bv[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        int bl[4] = {0, 1, 2, 3};
+        const uint32_t dbase = tmem + lane_base + db * kAsgMaxN;
+        for (int c0 = 0; c0 < Kc; c0 += 64) {
+          uint32_t v[64];
+          tmem_ld64(dbase + c0, v);
+          tmem_ld_wait();
+          // only the 16-column groups that hold centres (compile-time bodies: v stays in registers);
+          // columns past Kc in the last group read as -inf
+          const int nk = min(64, Kc - c0);
+          auto scan = [&](auto groups) {
+            constexpr int G16 = decltype(groups)::value;
+  #pragma unroll
+            for (int k = 0; k < 16 * G16; ++k) {
+              const float dv = (k < 16 * (G16 - 1) || k < nk) ? __uint_as_float(v[k]) : -INFINITY;
+              if (dv > bv[k & 3]) { bv[k & 3] = dv; bl[k & 3] = c0 + k; }
+            }
+          };
+          switch ((nk + 15) >> 4) {
+            case 1: scan(std::integral_constant<int, 1>{}); break;
+            case 2: scan(std::integral_constant<int, 2>{}); break;
+            case 3: scan(std::integral_constant<int, 3>{}); break;
+            default: scan(std::integral_constant<int, 4>{}); break;
           }
-        };
-        switch ((nk + 15) >> 4) {
-          case 1: scan(std::integral_constant<int, 1>{}); break;
-          case 2: scan(std::integral_constant<int, 2>{}); break;
-          case 3: scan(std::integral_constant<int, 3>{}); break;
-          default: scan(std::integral_constant<int, 4>{}); break;
+        }
+        float best = bv[0];
+        int lab = bl[0];
+  #pragma unroll
+        for (int s2 = 1; s2 < 4; ++s2)
+          if (bv[s2] > best || (bv[s2] == best && bl[s2] < lab)) { best = bv[s2]; lab = bl[s2]; }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&d_empty[db]);
+        if (px < p.n) {
+          const size_t pi = (size_t)f * p.n + px;
+          const bool covered = best >= tau2;
+          p.flags[flag_at(p, f, px)] = (uint8_t)((fl & ~PF_COVERED) | (covered ? PF_COVERED : 0));
+          p.labels[pi] = lab;
+          // warp-aggregated histogram: neighbouring pixels mostly share a label, and 32 same-address
+          // shared atomics would serialise
+          const unsigned same = __match_any_sync(__activemask(), lab);
+          if ((__ffs(same) - 1) == lane) atomicAdd(&shist[((fcount - 1) & 1) * kAsgMaxN + lab], __popc(same));
+          cand += (!covered && !(fl & PF_VISITED)) ? 1 : 0;
         }
       }
-      float best = bv[0];
-      int lab = bl[0];
-#pragma unroll
-      for (int s2 = 1; s2 < 4; ++s2)
-        if (bv[s2] > best || (bv[s2] == best && bl[s2] < lab)) { best = bv[s2]; lab = bl[s2]; }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&d_empty[db]);
-      const long long px = (long long)t * kBN + q * 32 + lane;
-      if (px < p.n) {
-        const size_t pi = (size_t)f * p.n + px;
-        const bool covered = best >= tau2;
-        p.flags[flag_at(p, f, px)] = (uint8_t)((fl & ~PF_COVERED) | (covered ? PF_COVERED : 0));
-        p.labels[pi] = lab;
-        // warp-aggregated histogram: neighbouring pixels mostly share a label, and 32 same-address
-        // shared atomics would serialise
-        const unsigned same = __match_any_sync(__activemask(), lab);
-        if ((__ffs(same) - 1) == lane) atomicAdd(&shist[((fcount - 1) & 1) * kAsgMaxN + lab], __popc(same));
-        cand += (!covered && !(fl & PF_VISITED)) ? 1 : 0;
-      }
+      n_act += s1 - s0;
+      flush(f, (fcount - 1) & 1);  // every epilogue warp flushes every active frame of the range
     }
-    if (last_f >= 0) flush(last_f, (fcount - 1) & 1);
   }
 
   tc_fence_before();

@@ -18,18 +18,32 @@ def launches(src, dst):
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[hi]
     ki, mi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    ni = hdr.index("Metric Name") if "Metric Name" in hdr else None
+    BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     tot, cnt = collections.defaultdict(float), collections.Counter()
+    dram = collections.defaultdict(float)
     for r in rows[hi + 1:]:
         if len(r) <= mi or not r[mi]:
             continue
-        us = float(r[mi].replace(",", "")) * UNIT.get(r[ui], 1.0)
         name = r[ki].split("(")[0].replace("void ", "").strip()
-        tot[name] += us
+        metric = r[ni] if ni is not None else "gpu__time_duration.sum"
+        v = float(r[mi].replace(",", ""))
+        if metric.startswith("dram__bytes"):
+            dram[name] += v * BYTES.get(r[ui], 1.0)
+            continue
+        if metric != "gpu__time_duration.sum":
+            continue
+        tot[name] += v * UNIT.get(r[ui], 1.0)
         cnt[name] += 1
     T = sum(tot.values())
-    out = ["| kernel | launches | total us | share | avg us |", "|---|---|---|---|---|"]
+    hd = bool(dram)
+    out = ["| kernel | launches | total us | share | avg us |" + (" DRAM MB / launch | DRAM GB/s |" if hd else ""),
+           "|---|---|---|---|---|" + ("---|---|" if hd else "")]
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
-        out.append(f"| `{k}` | {cnt[k]} | {v:.1f} | {100 * v / T:.1f}% | {v / cnt[k]:.2f} |")
+        row = f"| `{k}` | {cnt[k]} | {v:.1f} | {100 * v / T:.1f}% | {v / cnt[k]:.2f} |"
+        if hd:
+            row += f" {dram[k] / cnt[k] / 1e6:.1f} | {dram[k] / (v * 1e-6) / 1e9:.0f} |"
+        out.append(row)
     out.append(f"\nTotal device time over {sum(cnt.values())} launches: {T:.1f} us "
                "(ncu serialised, cold-cache per launch: compare shares, not absolutes).")
     open(dst, "w").write("\n".join(out) + "\n")
