@@ -22,13 +22,22 @@ __global__ void plan_kernel(Params p) {
   __shared__ int sm[33];
   __shared__ int s_tiles_total;
   int carry_t = 0;
+  long long units = 0, count_units = 0;  // active seeds this step (A_t) and converged modes counted
   for (int f0 = 0; f0 < p.B; f0 += blockDim.x) {
     const int f = f0 + threadIdx.x;
-    int nt = 0;
+    int nt = 0, u_it = 0, u_ct = 0;
     if (f < p.B) {
       FrameCtl& c = p.ctl[f];
-      if ((c.phase == PH_ITERATE || c.phase == PH_COUNT) && c.n_active > 0) nt = (c.n_active + kBM - 1) / kBM;
+      if ((c.phase == PH_ITERATE || c.phase == PH_COUNT) && c.n_active > 0) {
+        nt = (c.n_active + kBM - 1) / kBM;
+        (c.phase == PH_ITERATE ? u_it : u_ct) = c.n_active;
+      }
     }
+    int ti, tc;
+    block_excl_scan(u_it, sm, &ti);
+    block_excl_scan(u_ct, sm, &tc);
+    units += ti;
+    count_units += tc;
     int tt;
     const int ot = block_excl_scan(nt, sm, &tt);
     if (f < p.B) {
@@ -57,11 +66,6 @@ __global__ void plan_kernel(Params p) {
     p.counters[0] = s_tiles_total * p.n_chunks;
     p.counters[1] = s_tiles_total;
     p.counters[3] = 0;
-    long long units = 0, count_units = 0;
-    for (int f = 0; f < p.B; ++f) {
-      if (p.ctl[f].n_tiles_step && p.ctl[f].phase == PH_ITERATE) units += p.ctl[f].n_active;
-      if (p.ctl[f].n_tiles_step && p.ctl[f].phase == PH_COUNT) count_units += p.ctl[f].n_active;
-    }
     reinterpret_cast<long long*>(p.counters + 6)[0] = units;  // active seeds this step (A_t summed)
     reinterpret_cast<long long*>(p.counters + 10)[0] = count_units;  // converged modes counted (R10)
   }
