@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--kernel-profile", default="flat", choices=["flat", "gauss"],
                     help="kernel of the mean-shift update: the paper's flat kernel, or the Gaussian profile "
                          "(NEXT-4, reading R23; SFU-bound)")
+    ap.add_argument("--extras-budget-s", type=float, default=300.0,
+                    help="N > 1: time budget of the sharded extra measurements")
     ap.add_argument("--no-seed-shard", action="store_true",
                     help="with N > 1 replicas: skip the extra seed-sharded C4 measurement")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
@@ -371,21 +373,6 @@ def main():
         e2e = {"value": ksteps * B * (1 if sharded else world) / (ems / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": B * n * d * 4, "d2h_bytes_per_step": B * n * 4 + B * CAP * d * 4}
 
-    seed_sh = pix_sh = None
-    if world > 1 and not sharded and not args.no_seed_shard:
-        try:
-            seed_sh = seed_sharded_c4(world, rank, local)
-        except Exception as e:  # reported, not fatal: the replicas line above is the headline
-            seed_sh = {"error": f"{type(e).__name__}: {e}"[:300]}
-        try:
-            pix_sh = pixel_sharded_c5(world, rank, local)
-        except Exception as e:
-            pix_sh = {"error": f"{type(e).__name__}: {e}"[:300]}
-
-    if rank != 0:
-        if world > 1:
-            torch.distributed.destroy_process_group()
-        return
     peaks, src = measured_peaks()
     # algorithmic: 4 n D per active seed-iteration (similarity + weighted sum) and 2 n D
     # per converged mode in K2's intensity pass (similarity only, R10)
@@ -456,11 +443,28 @@ def main():
         "e2e": e2e,
         "cpu_baseline": cb,
     }
-    if seed_sh is not None:
-        line["seed_sharded"] = seed_sh
-    if pix_sh is not None:
-        line["pixel_sharded"] = pix_sh
-    print(json.dumps(line), flush=True)
+    if world > 1 and not sharded and not args.no_seed_shard:
+        # strong-scaling extras (C4 seed-sharded, C5 pixel-sharded) after the headline measurement; a
+        # watchdog prints the headline line and ends every rank if they overrun (a stuck collective
+        # must not cost the run its line)
+        import threading
+
+        def _overrun():
+            if rank == 0:
+                line["sharded_extras"] = "skipped: exceeded the time budget"
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+        guard = threading.Timer(args.extras_budget_s, _overrun)
+        guard.daemon = True
+        guard.start()
+        for key, fn in (("seed_sharded", seed_sharded_c4), ("pixel_sharded", pixel_sharded_c5)):
+            try:
+                line[key] = fn(world, rank, local)
+            except Exception as e:  # reported, not fatal: the replicas line is the headline
+                line[key] = {"error": f"{type(e).__name__}: {e}"[:300]}
+        guard.cancel()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
