@@ -38,10 +38,11 @@ class Policy(C.Structure):
                 ("L", C.c_double), ("H", C.c_double), ("P", C.c_double),
                 ("has_background", C.c_int32), ("min_instance_px", C.c_int32),
                 ("saturation_stop", C.c_int32), ("max_rounds", C.c_int32),
-                ("rng_seed", C.c_uint64), ("profile", C.c_int32), ("pad", C.c_int32)]
+                ("rng_seed", C.c_uint64), ("profile", C.c_int32), ("metric", C.c_int32)]
 
 
 PROFILE_FLAT, PROFILE_GAUSS = 0, 1
+METRIC_COSINE, METRIC_EUCLID = 0, 1
 
 
 class Trace(C.Structure):
@@ -112,9 +113,10 @@ def lib():
 
 
 def policy(kind=SEEDS_OSOP, n_seeds=128, gamma=0.9, L=2.0, H=8.0, P=0.99, has_background=1,
-           min_instance_px=0, saturation_stop=0, max_rounds=8, rng_seed=0, profile=PROFILE_FLAT) -> Policy:
+           min_instance_px=0, saturation_stop=0, max_rounds=8, rng_seed=0, profile=PROFILE_FLAT,
+           metric=METRIC_COSINE) -> Policy:
     return Policy(kind, n_seeds, gamma, L, H, P, has_background, min_instance_px, saturation_stop,
-                  max_rounds, rng_seed, profile, 0)
+                  max_rounds, rng_seed, profile, metric)
 
 
 @dataclass

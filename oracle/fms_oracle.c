@@ -201,7 +201,38 @@ int32_t fmso_lockstep(const double* xhat, int64_t n, int32_t d, double h, int32_
 int32_t fmso_lockstep_p(const double* xhat, int64_t n, int32_t d, double h, int32_t max_iter,
                         double tol, double gamma, int64_t K, double* seeds, uint8_t* status,
                         int64_t* intensity, int32_t* iters, int64_t* seed_iters, int32_t profile) {
+  return fmso_lockstep_m(xhat, n, d, h, max_iter, tol, gamma, K, seeds, status, intensity, iters, seed_iters,
+                         profile, FMSO_METRIC_COSINE);
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * NEXT-4, reading R24: Eq. 3's flat kernel with the Euclidean distance of Eq. 4, which
+ * Eq. 9 replaces on the paper's cosine path:
+ *     S_h(s) = { x_i : |x_i - s|_2 <= h },   m_h(s) = (1/|S_h(s)|) sum_{S_h(s)} x_i   (Eq. 8 / 10)
+ * on the raw embeddings (no normalisation, no renormalisation of the shifted seed).
+ * ------------------------------------------------------------------------------------------- */
+int64_t fmso_window_euclid(const double* x, int64_t n, int32_t d, double h, const double* s, double* g) {
+  int64_t cnt = 0;
+  const double h2 = h * h;
+  for (int32_t k = 0; k < d; ++k) g[k] = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double* xi = x + i * d;
+    double d2 = 0.0;
+    for (int32_t k = 0; k < d; ++k) d2 += (xi[k] - s[k]) * (xi[k] - s[k]);
+    if (d2 <= h2) {
+      for (int32_t k = 0; k < d; ++k) g[k] += xi[k];
+      ++cnt;
+    }
+  }
+  return cnt;
+}
+
+int32_t fmso_lockstep_m(const double* xhat, int64_t n, int32_t d, double h, int32_t max_iter,
+                        double tol, double gamma, int64_t K, double* seeds, uint8_t* status,
+                        int64_t* intensity, int32_t* iters, int64_t* seed_iters, int32_t profile,
+                        int32_t metric) {
   const double tau = 1.0 - h;
+  const int euclid = metric == FMSO_METRIC_EUCLID;
   const int32_t need = fmso_need(gamma, K);
   int32_t t_run = 0;
   *seed_iters = 0;
@@ -217,12 +248,13 @@ int32_t fmso_lockstep_p(const double* xhat, int64_t n, int32_t d, double h, int3
       if (status[j] != 0) continue;
       double g[256], sn[256];
       double* s = seeds + j * d;
-      const double mass = profile == FMSO_PROFILE_GAUSS ? fmso_window_gauss(xhat, n, d, h, s, g)
-                                                         : (double)fmso_window(xhat, n, d, tau, s, g);
+      const double mass = euclid ? (double)fmso_window_euclid(xhat, n, d, h, s, g)
+                          : profile == FMSO_PROFILE_GAUSS ? fmso_window_gauss(xhat, n, d, h, s, g)
+                                                          : (double)fmso_window(xhat, n, d, tau, s, g);
       if (mass == 0.0) { status[j] = 2; continue; }
       double nn = 0.0;
       for (int32_t k = 0; k < d; ++k) nn += g[k] * g[k];
-      nn = sqrt(nn);
+      nn = euclid ? mass : sqrt(nn);  /* Euclidean: the window mean; cosine: onto the sphere (R4) */
       double dd = 0.0;
       for (int32_t k = 0; k < d; ++k) {
         sn[k] = g[k] / nn;
@@ -244,7 +276,8 @@ int32_t fmso_lockstep_p(const double* xhat, int64_t n, int32_t d, double h, int3
   for (int64_t j = 0; j < K; ++j) {
     if (status[j] != 1) continue;
     double g[256];
-    intensity[j] = fmso_window(xhat, n, d, tau, seeds + j * d, g);
+    intensity[j] = euclid ? fmso_window_euclid(xhat, n, d, h, seeds + j * d, g)
+                          : fmso_window(xhat, n, d, tau, seeds + j * d, g);
   }
   return t_run;
 }
@@ -267,6 +300,11 @@ static int cmp_mrank(const void* a, const void* b) {
 
 int64_t fmso_merge(const double* pool, const int64_t* intensity, const int64_t* origin, int64_t m,
                    int32_t d, double rho, int64_t* keep) {
+  return fmso_merge_m(pool, intensity, origin, m, d, rho, keep, FMSO_METRIC_COSINE);
+}
+
+int64_t fmso_merge_m(const double* pool, const int64_t* intensity, const int64_t* origin, int64_t m,
+                     int32_t d, double rho, int64_t* keep, int32_t metric) {
   mrank_t* ord = (mrank_t*)malloc((size_t)(m > 0 ? m : 1) * sizeof(mrank_t));
   for (int64_t j = 0; j < m; ++j) { ord[j].inten = intensity[j]; ord[j].origin = origin[j]; ord[j].idx = j; }
   qsort(ord, (size_t)m, sizeof(mrank_t), cmp_mrank);
@@ -276,9 +314,15 @@ int64_t fmso_merge(const double* pool, const int64_t* intensity, const int64_t* 
     int ok = 1;
     for (int64_t q = 0; q < kept && ok; ++q) {
       const double* b = pool + keep[q] * d;
-      double dot = 0.0;
-      for (int32_t k = 0; k < d; ++k) dot += a[k] * b[k];
-      if (1.0 - dot <= rho) ok = 0;
+      if (metric == FMSO_METRIC_EUCLID) {
+        double d2 = 0.0;
+        for (int32_t k = 0; k < d; ++k) d2 += (a[k] - b[k]) * (a[k] - b[k]);
+        if (d2 <= rho * rho) ok = 0;
+      } else {
+        double dot = 0.0;
+        for (int32_t k = 0; k < d; ++k) dot += a[k] * b[k];
+        if (1.0 - dot <= rho) ok = 0;
+      }
     }
     if (ok) keep[kept++] = ord[o].idx;
   }
@@ -310,6 +354,29 @@ void fmso_assign(const double* xhat, int64_t n, int32_t d, const double* centres
   for (int64_t i = 0; i < n; ++i) hist[labels[i]]++;
 }
 
+void fmso_assign_m(const double* x, int64_t n, int32_t d, const double* centres, int64_t K, double h,
+                   int32_t* labels, uint8_t* covered, int64_t* hist, int32_t metric) {
+  if (metric != FMSO_METRIC_EUCLID) {
+    fmso_assign(x, n, d, centres, K, 1.0 - h, labels, covered, hist);
+    return;
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    const double* xi = x + i * d;
+    double best = INFINITY;
+    int32_t lab = 0;
+    for (int64_t k = 0; k < K; ++k) {
+      double d2 = 0.0;
+      for (int32_t q = 0; q < d; ++q) d2 += (xi[q] - centres[k * d + q]) * (xi[q] - centres[k * d + q]);
+      if (d2 < best) { best = d2; lab = (int32_t)k; }
+    }
+    labels[i] = lab;
+    covered[i] = best <= h * h ? 1 : 0;
+  }
+  for (int64_t k = 0; k < K; ++k) hist[k] = 0;
+  for (int64_t i = 0; i < n; ++i) hist[labels[i]]++;
+}
+
 /* ---------------------------------------------------------------------------------------------
  * The whole method: Alg. 2 wrapped in the OSOP controller of Fig. 3 / P:316-318.
  *   round 0: K_0 = N_initial (OSOP), n_seeds (FIXED) or n (ALL = Alg. 1, gamma = 1)
@@ -323,8 +390,11 @@ void fmso_assign(const double* xhat, int64_t n, int32_t d, const double* centres
 int fmso_cluster(const float* emb, int64_t n, int32_t d, double h, int32_t max_iter, double tol,
                  const fmso_policy* pol, int32_t* labels, double* centres, int32_t centres_cap,
                  int32_t* K_out, fmso_trace* trace) {
-  if (n < 1 || d < 1 || d > 256 || !(h > 0.0 && h < 1.0) || !(tol > 0.0) || max_iter < 1 || !pol)
+  if (!pol) return FMSO_E_INVALID;
+  const int euclid = pol->metric == FMSO_METRIC_EUCLID;
+  if (n < 1 || d < 1 || d > 256 || !(h > 0.0 && (euclid || h < 1.0)) || !(tol > 0.0) || max_iter < 1)
     return FMSO_E_INVALID;
+  if (pol->metric != FMSO_METRIC_COSINE && (!euclid || pol->profile != FMSO_PROFILE_FLAT)) return FMSO_E_INVALID;
   if (pol->kind < 0 || pol->kind > 2 || pol->max_rounds < 1 || pol->max_rounds > FMSO_MAX_ROUNDS)
     return FMSO_E_INVALID;
   if (pol->kind != FMSO_SEEDS_ALL && pol->n_seeds < 1) return FMSO_E_INVALID;
@@ -350,8 +420,12 @@ int fmso_cluster(const float* emb, int64_t n, int32_t d, double h, int32_t max_i
   fmso_trace tr;
   memset(&tr, 0, sizeof(tr));
 
-  rc = fmso_normalize(emb, n, d, xhat);
-  if (rc != FMSO_OK) goto done;
+  if (euclid) {  /* R24: the raw embeddings (Eq. 4 needs no normalisation) */
+    for (int64_t i = 0; i < n * d; ++i) xhat[i] = (double)emb[i];
+  } else {
+    rc = fmso_normalize(emb, n, d, xhat);
+    if (rc != FMSO_OK) goto done;
+  }
 
   int64_t total = 0, K_next = 0;
   int32_t I_prev = -1;
@@ -373,8 +447,8 @@ int fmso_cluster(const float* emb, int64_t n, int32_t d, double h, int32_t max_i
     for (int64_t j = 0; j < Kr; ++j) memcpy(seeds + j * d, xhat + idx[j] * d, (size_t)d * sizeof(double));
     double gam = pol->kind == FMSO_SEEDS_ALL ? 1.0 : pol->gamma;
     int64_t sit = 0;
-    int32_t t_run = fmso_lockstep_p(xhat, n, d, h, max_iter, tol, gam, Kr, seeds, st, inten, its, &sit,
-                                    pol->profile);
+    int32_t t_run = fmso_lockstep_m(xhat, n, d, h, max_iter, tol, gam, Kr, seeds, st, inten, its, &sit,
+                                    pol->profile, pol->metric);
 
     int64_t nconv = 0, ndisc = 0;
     for (int64_t j = 0; j < Kr; ++j) { nconv += st[j] == 1; ndisc += st[j] != 1; }
@@ -410,7 +484,7 @@ int fmso_cluster(const float* emb, int64_t n, int32_t d, double h, int32_t max_i
         porg[p] = idx[j];
         ++p;
       }
-    int64_t kept = fmso_merge(pool, pint, porg, m, d, rho, keep);
+    int64_t kept = fmso_merge_m(pool, pint, porg, m, d, rho, keep, pol->metric);
     if (kept > cap) {
       cap = kept * 2;
       cvec = (double*)realloc(cvec, (size_t)cap * d * sizeof(double));
@@ -429,7 +503,7 @@ int fmso_cluster(const float* emb, int64_t n, int32_t d, double h, int32_t max_i
     /* assign every pixel to its nearest centre */
     free(hist);
     hist = (int64_t*)malloc((size_t)Kc * sizeof(int64_t));
-    fmso_assign(xhat, n, d, cvec, Kc, tau, labels, covered, hist);
+    fmso_assign_m(xhat, n, d, cvec, Kc, h, labels, covered, hist, pol->metric);
     int64_t ncand2 = 0;
     for (int64_t i = 0; i < n; ++i) ncand2 += (!covered[i] && !visited[i]);
     tr.round_Kc[round] = (int32_t)Kc;

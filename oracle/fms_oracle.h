@@ -33,9 +33,11 @@ typedef struct {
   uint64_t rng_seed;       /* hash-priority selection salt (R11) */
   int32_t profile;         /* kernel profile of the iteration: FMSO_PROFILE_FLAT (Eq. 3/11, the paper) or
                               FMSO_PROFILE_GAUSS (NEXT-4, reading R23) */
-  int32_t pad;
+  int32_t metric;          /* FMSO_METRIC_COSINE (Eq. 9, the paper's path) or FMSO_METRIC_EUCLID (Eq. 4,
+                              NEXT-4, reading R24; flat profile only) */
 } fmso_policy;
 enum { FMSO_PROFILE_FLAT = 0, FMSO_PROFILE_GAUSS = 1 };
+enum { FMSO_METRIC_COSINE = 0, FMSO_METRIC_EUCLID = 1 };
 
 typedef struct {
   int32_t rounds, K;
@@ -78,6 +80,22 @@ double fmso_window_gauss(const double* xhat, int64_t n, int32_t d, double h, con
 int32_t fmso_lockstep_p(const double* xhat, int64_t n, int32_t d, double h, int32_t max_iter,
                         double tol, double gamma, int64_t K, double* seeds, uint8_t* status,
                         int64_t* intensity, int32_t* iters, int64_t* seed_iters, int32_t profile);
+/* NEXT-4, reading R24: the Euclidean metric of Eq. 4 with the flat kernel of Eq. 3 on the
+ * raw (unnormalised) embeddings: S_h(s) = { x_i : |x_i - s|_2 <= h } (inclusive), g = sum x_i
+ * (ascending i); returns |S_h(s)|.  The mean-shift update is then the window mean g / |S_h(s)|. */
+int64_t fmso_window_euclid(const double* x, int64_t n, int32_t d, double h, const double* s, double* g);
+/* fmso_lockstep_p with the metric selectable (FMSO_METRIC_*; Euclidean needs the flat profile): the
+ * Euclidean update is s' = g / |S_h(s)| without renormalisation, convergence |s' - s|_2 < tol. */
+int32_t fmso_lockstep_m(const double* x, int64_t n, int32_t d, double h, int32_t max_iter, double tol,
+                        double gamma, int64_t K, double* seeds, uint8_t* status, int64_t* intensity,
+                        int32_t* iters, int64_t* seed_iters, int32_t profile, int32_t metric);
+/* Greedy merge with the metric selectable: Euclidean keeps a mode unless |m - c|_2 <= rho. */
+int64_t fmso_merge_m(const double* pool, const int64_t* intensity, const int64_t* origin, int64_t m,
+                     int32_t d, double rho, int64_t* keep, int32_t metric);
+/* Assignment with the metric selectable: Euclidean label = argmin_k |x - c_k|_2 (lowest k on ties),
+ * covered = min_k |x - c_k|_2 <= h.  (Cosine: fmso_assign with tau = 1 - h.) */
+void fmso_assign_m(const double* x, int64_t n, int32_t d, const double* centres, int64_t K, double h,
+                   int32_t* labels, uint8_t* covered, int64_t* hist, int32_t metric);
 /* Lockstep mean-shift over K seeds (Alg. 2 l.4-9 + early stop).  seeds[K*d] in/out, status[K]:
  * 1 converged, 2 stalled, 3 discarded.  Returns iterations run; writes, for converged seeds, the
  * intensity |S_h(m)| (flat-kernel density of Eq. 2 at the mode, R10) and per-seed iterations. */
