@@ -157,7 +157,13 @@ fms_status fms_set_pixel_shard(void* ctx, fms_exchange_fn fn, void* user, int32_
  *          DESIGN reading R23): Eq. 2's k(t) = exp(-t/2) at t = |x - s|^2 / h, i.e. every pixel
  *          weighs w = exp(-(1 - x.s)/h) in s' = normalize(sum_i w_i x_i) (fp16 weights; weights
  *          below 2^-24 flush to zero).  Intensity, merge, coverage and assignment keep the flat
- *          window in both.  Pixel sharding requires 0 (FMS_E_INVALID at the clustering call). */
+ *          window in both.  Pixel sharding requires 0 (FMS_E_INVALID at the clustering call).
+ *          "metric" (0/1, default 0): 0 = cosine distance on normalised embeddings (Eq. 9, the paper's
+ *          path).  1 = Euclidean distance (Eq. 4, DESIGN reading R24): the
+ *          raw embeddings, window |x - s|_2 <= bandwidth (any bandwidth > 0), update = window mean
+ *          (no renormalisation), merge radius and coverage radius = bandwidth, label = nearest centre
+ *          in L2; zero vectors are valid.  Needs d <= 30, kernel_profile 0 and no pixel sharding
+ *          (FMS_E_INVALID otherwise).  centres come back in the caller's units. */
 fms_status fms_set_option(void* ctx, const char* key, int64_t value);
 
 /* Cluster one frame.  emb: device, [n][d] fp32 row-major.  labels: device int32[n] in [0, K).

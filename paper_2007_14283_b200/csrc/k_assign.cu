@@ -113,11 +113,15 @@ __global__ void __launch_bounds__(kAsgThreads, 1) assign_tc_kernel(const __grid_
         for (int idx = lane; idx < n_rows * (DP / 8); idx += 32) {  // one 8-feature chunk per step
           const int r = idx / (DP / 8), ch = idx - r * (DP / 8);
           __align__(16) __half hi[8], hs[8], lo[8];
+          float row[DP];  // the centre's operand row (augmented for the Euclidean metric, R24)
+          if (r < Kc) {
+            operand_row<DP>(p, f, cent + (size_t)r * DP, row);
+          } else {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float v = r < Kc ? cent[(size_t)r * DP + ch * 8 + e] : 0.f;
-            split_seed(v, hi[e], hs[e], lo[e]);
+            for (int e = 0; e < DP; ++e) row[e] = 0.f;
           }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) split_seed(row[ch * 8 + e], hi[e], hs[e], lo[e]);
           const uint32_t off = swz_off<DP>(r, ch);
           *reinterpret_cast<uint4*>(dst + off) = *reinterpret_cast<const uint4*>(hi);
           *reinterpret_cast<uint4*>(dst + Cfg::CEN_B + off) = *reinterpret_cast<const uint4*>(hs);

@@ -93,6 +93,15 @@ __device__ void merge_nms(const Params& p, int f, const int* vals, int P, float*
   const int* porg = p.porg + (size_t)f * p.P_cap;
   float* cent = p.cent + (size_t)f * p.C_cap * DP;
   const float thr = p.rho_f;  // keep unless x.c >= 1 - rho
+  // Euclidean (R24): keep unless |m - c| <= rho = h, in the frame's scaled units
+  const float rho2 = p.metric == 1 ? (float)((double)p.fscale[f] * p.h * (double)p.fscale[f] * p.h) : 0.f;
+  auto close = [&](const float* a, const float* b) -> bool {
+    if (p.metric != 1) return dotv<DP>(a, b) >= thr;
+    float d2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < DP; ++k) d2 = fmaf(a[k] - b[k], a[k] - b[k], d2);
+    return d2 <= rho2;
+  };
   if (threadIdx.x == 0) { s_kept = 0; s_err = 0; }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -110,12 +119,12 @@ __device__ void merge_nms(const Params& p, int f, const int* vals, int P, float*
     for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
       const int ci = idx / kept, k = idx - ci * kept;
       const float* kv = k < kKeptSm ? keptv + k * DP : cent + (size_t)k * DP;
-      if (dotv<DP>(cand + ci * DP, kv) >= thr) atomicOr(&s_supp, 1u << ci);
+      if (close(cand + ci * DP, kv)) atomicOr(&s_supp, 1u << ci);
     }
     // all in-batch pairs (i, j < i) at once, one per thread, instead of a serial loop per lane
     for (int idx = threadIdx.x; idx < 32 * 32; idx += blockDim.x) {
       const int i = idx >> 5, j = idx & 31;
-      if (i < nb && j < i && dotv<DP>(cand + i * DP, cand + j * DP) >= thr) atomicOr(&s_inb[i], 1u << j);
+      if (i < nb && j < i && close(cand + i * DP, cand + j * DP)) atomicOr(&s_inb[i], 1u << j);
     }
     __syncthreads();
     if (warp == 0) {
@@ -232,11 +241,13 @@ __global__ void __launch_bounds__(256) assign_kernel(Params p) {
   float x[DP];
 #pragma unroll
   for (int k = 0; k < DP; ++k) x[k] = 0.f;
+  const bool euclid = p.metric == 1;
+  const float sg = euclid ? p.fscale[f] : 1.f;
   if (valid) {
     const float* src = p.emb + ((size_t)f * p.n + i) * p.d;
 #pragma unroll
     for (int k = 0; k < DP; ++k)
-      if (k < p.d) x[k] = src[k];
+      if (k < p.d) x[k] = src[k] * sg;
   }
   if (threadIdx.x == 0) s_cand = 0;
   float best = -INFINITY;
@@ -248,7 +259,9 @@ __global__ void __launch_bounds__(256) assign_kernel(Params p) {
     for (int t = threadIdx.x; t < nk * DP; t += blockDim.x) sc[t] = cent[(size_t)k0 * DP + t];
     __syncthreads();
     for (int k = 0; k < nk; ++k) {
-      const float dv = dotv<DP>(x, sc + k * DP);
+      // Euclidean (R24): rank by x.c - |c|^2 / 2 = (|x|^2 - |x - c|^2) / 2
+      const float dv = euclid ? dotv<DP>(x, sc + k * DP) - 0.5f * dotv<DP>(sc + k * DP, sc + k * DP)
+                              : dotv<DP>(x, sc + k * DP);
       if (dv > best) { best = dv; lab = k0 + k; }
     }
   }
@@ -256,7 +269,8 @@ __global__ void __launch_bounds__(256) assign_kernel(Params p) {
   int cand = 0;
   if (valid) {
     const size_t pi = (size_t)f * p.n + i;
-    const bool covered = best * p.inv[pi] >= p.tau_f;
+    const double hs = (double)sg * p.h;
+    const bool covered = euclid ? best >= 0.5f * (dotv<DP>(x, x) - (float)(hs * hs)) : best * p.inv[pi] >= p.tau_f;
     const uint8_t fl = p.flags[flag_at(p, f, i)];
     p.flags[flag_at(p, f, i)] = (uint8_t)((fl & ~PF_COVERED) | (covered ? PF_COVERED : 0));
     p.labels[pi] = lab;
@@ -343,7 +357,9 @@ __global__ void output_kernel(Params p, float* centres_out, int cap) {
   const int Kc = c.Kc < cap ? c.Kc : cap;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < Kc * p.d; t += gridDim.x * blockDim.x) {
     const int k = t / p.d, q = t - k * p.d;
-    centres_out[((size_t)f * cap + k) * p.d + q] = p.cent[((size_t)f * p.C_cap + k) * DP + q];
+    // Euclidean: back to the caller's units (1 / sigma is a power of two: exact)
+    centres_out[((size_t)f * cap + k) * p.d + q] =
+        p.cent[((size_t)f * p.C_cap + k) * DP + q] * (p.metric == 1 ? 1.f / p.fscale[f] : 1.f);
   }
 }
 

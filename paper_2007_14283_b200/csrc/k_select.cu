@@ -28,6 +28,66 @@ __global__ void init_ctl_kernel(Params p) {
   for (int r = 0; r < kMaxRounds; ++r) c.round_nmin[r] = 0.0;
 }
 
+// Euclidean metric: per-frame max |x|^2 (float bits, non-negative: integer order = float order)
+__global__ void maxnorm_kernel(Params p) {
+  const int f = blockIdx.y;
+  float m = 0.f;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += (long long)gridDim.x * blockDim.x) {
+    const float* x = p.emb + ((size_t)f * p.n + i) * p.d;
+    float ss = 0.f;
+    for (int k = 0; k < p.d; ++k) ss = fmaf(x[k], x[k], ss);
+    m = fmaxf(m, isfinite(ss) ? ss : INFINITY);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned*>(p.fscale) + f, __float_as_uint(m));
+}
+// max |x|^2 -> sigma = 2^-e with sqrt(max) < 2^e (power of two: scaling is exact)
+__global__ void scale_kernel(Params p) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= p.B) return;
+  const float m2 = p.fscale[f];
+  if (!isfinite(m2)) { p.ctl[f].status = 3; p.fscale[f] = 1.f; return; }  // non-finite input
+  int e = 0;
+  frexpf(sqrtf(m2) * 1.0001f, &e);  // m < 2^e (the margin covers the fp32 rounding of the norm)
+  p.fscale[f] = m2 > 0.f ? ldexpf(1.f, -e) : 1.f;
+}
+
+template <int DP>
+__global__ void prep_euclid_kernel(Params p) {
+  const int f = blockIdx.y;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n_pad) return;
+  __align__(16) __half h[DP];
+  __align__(16) __half l[DP];
+  if (i < p.n) {
+    const float sg = p.fscale[f];
+    const float* x = p.emb + ((size_t)f * p.n + i) * p.d;
+    float v[DP];
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < DP; ++k) {
+      v[k] = k < p.d ? x[k] * sg : 0.f;
+      ss = fmaf(v[k], v[k], ss);
+    }
+    v[p.d] = -0.5f * ss;
+    v[p.d + 1] = 1.f;
+#pragma unroll
+    for (int k = 0; k < DP; ++k) limbs(v[k], h[k], l[k]);
+    p.inv[(size_t)f * p.n + i] = sg;  // seeds start at sigma x_i (select)
+    p.flags[flag_at(p, f, i)] = 0;
+  } else {
+#pragma unroll
+    for (int k = 0; k < DP; ++k) h[k] = l[k] = __float2half_rn(0.f);
+  }
+  uint4* dst = reinterpret_cast<uint4*>(p.Xh + ((size_t)f * p.n_pad + i) * DP);
+  uint4* dstl = reinterpret_cast<uint4*>(p.Xl + ((size_t)f * p.n_pad + i) * DP);
+#pragma unroll
+  for (int k = 0; k < DP / 8; ++k) {
+    dst[k] = reinterpret_cast<const uint4*>(h)[k];
+    dstl[k] = reinterpret_cast<const uint4*>(l)[k];
+  }
+}
+
 template <int DP>
 __global__ void prep_kernel(Params p) {
   const int f = blockIdx.y;
@@ -265,12 +325,15 @@ __global__ void sel_write_kernel(Params p) {
     const bool own = pos % p.world == p.rank;
     const int lp = pos / p.world;
     __align__(16) __half sh[DP], ss[DP], sl[DP];
+    float sv[DP], row[DP];
 #pragma unroll
     for (int k = 0; k < DP; ++k) {
-      float v = (have && k < p.d) ? x[k] * inv : 0.f;
-      s[k] = v;
-      split_seed(v, sh[k], ss[k], sl[k]);
+      sv[k] = (have && k < p.d) ? x[k] * inv : 0.f;
+      s[k] = sv[k];
     }
+    operand_row<DP>(p, f, sv, row);
+#pragma unroll
+    for (int k = 0; k < DP; ++k) split_seed(row[k], sh[k], ss[k], sl[k]);
     if (own) {
       const size_t ro = (size_t)f * p.S_pad + lp;
 #pragma unroll
@@ -324,6 +387,14 @@ __global__ void sel_finish_kernel(Params p) {
 cudaError_t launch_prep(const Params& p, cudaStream_t st) {
   init_ctl_kernel<<<(p.B + 127) / 128, 128, 0, st>>>(p);
   dim3 g((unsigned)((p.n_pad + 255) / 256), p.B);
+  if (p.metric == 1) {
+    cudaMemsetAsync(p.fscale, 0, (size_t)p.B * 4, st);
+    maxnorm_kernel<<<dim3(64, p.B), 256, 0, st>>>(p);
+    scale_kernel<<<(p.B + 127) / 128, 128, 0, st>>>(p);
+    if (p.DP == 16) prep_euclid_kernel<16><<<g, 256, 0, st>>>(p);
+    else prep_euclid_kernel<32><<<g, 256, 0, st>>>(p);
+    return cudaGetLastError();
+  }
   if (p.DP == 16) prep_kernel<16><<<g, 256, 0, st>>>(p);
   else prep_kernel<32><<<g, 256, 0, st>>>(p);
   return cudaGetLastError();

@@ -70,12 +70,15 @@ __global__ void psel_unpack_kernel(Params p) {
     const int* row = p.pbuf + ((size_t)f * p.pkmax + j) * DP;
     float* s = p.seeds + ((size_t)f * p.S_cap + j) * DP;
     __align__(16) __half sh[DP], ss[DP], sl[DP];
+    float sv[DP], orow[DP];
 #pragma unroll
     for (int k = 0; k < DP; ++k) {
-      const float v = __int_as_float(row[k]);
-      s[k] = v;
-      split_seed(v, sh[k], ss[k], sl[k]);
+      sv[k] = __int_as_float(row[k]);
+      s[k] = sv[k];
     }
+    operand_row<DP>(p, f, sv, orow);
+#pragma unroll
+    for (int k = 0; k < DP; ++k) split_seed(orow[k], sh[k], ss[k], sl[k]);
     const size_t ro = (size_t)f * p.S_pad + j;
 #pragma unroll
     for (int k = 0; k < DP / 8; ++k) {

@@ -91,7 +91,30 @@ __global__ void __launch_bounds__(kBM) update_kernel(Params p) {
         g[k] = p.gacc[r * DP + k];
         p.gacc[r * DP + k] = 0.0;  // every row of a processed tile is reset for the next step
       }
-      if (j < c.n_active) {
+      if (j < c.n_active && p.metric == 1) {
+        // Euclidean (R24): s' = window mean = G[0, d) / G[d + 1] (the ones column counts the window,
+        // both scaled by 2^11); no renormalisation; tolerance in the frame's scaled units
+        const size_t sidx = (size_t)task.f * p.S_cap + p.act[(size_t)task.f * p.S_cap + j];
+        const double cntw = g[p.d + 1];
+        if (!(cntw > 0.0)) {
+          p.sstat[sidx] = ST_STALLED;
+          stall = 1;
+        } else {
+          float* s = p.seeds + sidx * DP;
+          double dd = 0.0;
+#pragma unroll
+          for (int k = 0; k < DP; ++k) {
+            const double v = k < p.d ? g[k] / cntw : 0.0;
+            const double e = v - (double)s[k];
+            dd += e * e;
+            s[k] = (float)v;
+          }
+          if (sqrt(dd) < p.tol * (double)p.fscale[task.f]) {
+            p.sstat[sidx] = ST_CONV;
+            conv = 1;
+          }
+        }
+      } else if (j < c.n_active) {
         const size_t sidx = (size_t)task.f * p.S_cap + p.act[(size_t)task.f * p.S_cap + j];
         double nn = 0.0;
 #pragma unroll
@@ -144,8 +167,10 @@ __device__ int compact_seeds(const Params& p, int f, int K, uint8_t want, int* s
       __align__(16) __half h[DP];
       __align__(16) __half hs[DP];
       __align__(16) __half l[DP];
+      float row[DP];
+      operand_row<DP>(p, f, s, row);
 #pragma unroll
-      for (int k = 0; k < DP; ++k) split_seed(s[k], h[k], hs[k], l[k]);
+      for (int k = 0; k < DP; ++k) split_seed(row[k], h[k], hs[k], l[k]);
       const size_t ro = (size_t)f * p.S_pad + pos;
       uint4* dst = reinterpret_cast<uint4*>(p.sop + ro * DP);
       uint4* dsts = reinterpret_cast<uint4*>(p.sops + ro * DP);

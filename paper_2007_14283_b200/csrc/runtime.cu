@@ -96,6 +96,7 @@ struct Ctx {
   size_t pbuf_bytes = 0;
   int poll = kPoll;  // lockstep steps between host polls ("poll_steps")
   int kprofile = 0;  // "kernel_profile": 0 flat (the paper), 1 Gaussian (NEXT-4)
+  int metric = 0;    // "metric": 0 cosine (the paper's path), 1 Euclidean (NEXT-4)
   // host-buffer entry: chunked, double-buffered staging on a copy stream ("host_chunk")
   int host_chunk = 32;
   cudaStream_t cstream = nullptr;
@@ -138,7 +139,13 @@ fms_status validate(Ctx* c, int32_t B, int64_t n, int32_t d, double h, int32_t m
                     const fms_seed_policy* pol) {
   if (!c) return FMS_E_INVALID;
   if (B < 1 || n < 1 || d < 1 || d > 32) return fail(c, FMS_E_INVALID, "need B>=1, n>=1, 1<=d<=32");
-  if (!(h > 0.0 && h < 1.0)) return fail(c, FMS_E_INVALID, "bandwidth must be in (0,1) (cosine distance)");
+  if (c->metric == 1) {
+    if (d > 30) return fail(c, FMS_E_INVALID, "the Euclidean metric needs d <= 30 (two augmented columns)");
+    if (!(h > 0.0 && std::isfinite(h))) return fail(c, FMS_E_INVALID, "bandwidth must be > 0");
+    if (c->kprofile != 0) return fail(c, FMS_E_INVALID, "the Euclidean metric uses the flat kernel");
+  } else if (!(h > 0.0 && h < 1.0)) {
+    return fail(c, FMS_E_INVALID, "bandwidth must be in (0,1) (cosine distance)");
+  }
   if (!(tol > 0.0) || max_iters < 1) return fail(c, FMS_E_INVALID, "need tol>0 and max_iters>=1");
   if (!pol) return fail(c, FMS_E_INVALID, "policy is NULL");
   if (pol->kind < 0 || pol->kind > 2) return fail(c, FMS_E_INVALID, "bad policy kind");
@@ -188,6 +195,7 @@ size_t carve(Params& p, uint8_t* base) {
   p.sample = (unsigned long long*)take(B * (size_t)p.sample_cap * 8);
   p.blkcnt = (int*)take(B * (size_t)p.nblk_glob * 4);
   p.ctl = (FrameCtl*)take(B * sizeof(FrameCtl));
+  p.fscale = (float*)take(B * 4);
   if (p.P_cap > kMaxPcap) {  // merge pool sorted in global memory (Alg. 1)
     p.mkeys = (unsigned long long*)take(B * (size_t)p.P_cap * 8);
     p.mkeys_sorted = (unsigned long long*)take(B * (size_t)p.P_cap * 8);
@@ -222,7 +230,8 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   Params p{};
   p.B = B;
   p.d = d;
-  p.DP = d <= 16 ? 16 : 32;
+  p.DP = d + (c->metric == 1 ? 2 : 0) <= 16 ? 16 : 32;
+  p.metric = c->metric;
   p.max_iter = max_iters;
   p.n = n;
   p.n_pad = (long long)align_up((size_t)n, kBN);
@@ -232,6 +241,8 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
     return fail(c, FMS_E_INVALID, "pixel shard [offset, offset + n) outside the frame of n_global pixels");
   if (pshard && c->kprofile != 0)
     return fail(c, FMS_E_INVALID, "pixel sharding needs the flat kernel (its window sums are exchanged exactly)");
+  if (pshard && c->metric != 0)
+    return fail(c, FMS_E_INVALID, "pixel sharding needs the cosine metric (the Euclidean scale is per frame)");
   p.profile = c->kprofile;
   p.n_glob = pshard ? c->pn_glob : n;
   p.pix_off = pshard ? c->poff : 0;
@@ -255,7 +266,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   p.nblk = (int)((n + 2047) / 2048);
   p.h = h;
   p.tau = 1.0 - h;
-  p.tau_f = (float)(1.0 - h);
+  p.tau_f = c->metric == 1 ? kEuclidT0 : (float)(1.0 - h);  // Euclidean: rows carry the threshold
   p.rho_f = (float)(1.0 - h);  // merge radius rho = h (R10): keep unless x.c >= 1 - rho
   p.tol = tol;
   p.kind = pol->kind;
@@ -644,6 +655,11 @@ fms_status fms_set_option(void* ctx, const char* key, int64_t value) {
   if (!strcmp(key, "host_chunk")) {  // frames per chunk of fms_cluster_batch_host
     if (value < 1 || value > 1 << 20) return fail(c, FMS_E_INVALID, "host_chunk must be >= 1");
     c->host_chunk = (int)value;
+    return FMS_OK;
+  }
+  if (!strcmp(key, "metric")) {
+    if (value < 0 || value > 1) return fail(c, FMS_E_INVALID, "metric must be 0 (cosine) or 1 (Euclidean)");
+    c->metric = (int)value;
     return FMS_OK;
   }
   if (!strcmp(key, "kernel_profile")) {
