@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--kernel-profile", default="flat", choices=["flat", "gauss"],
                     help="kernel of the mean-shift update: the paper's flat kernel, or the Gaussian profile "
                          "(NEXT-4, reading R23; SFU-bound)")
+    ap.add_argument("--metric", default="cosine", choices=["cosine", "euclid"],
+                    help="euclid (NEXT-4, reading R24): the C2 frames row-normalised, Euclidean window "
+                         "sqrt(2h) (the same windows as cosine h at the start), window-mean update")
     ap.add_argument("--extras-budget-s", type=float, default=300.0,
                     help="N > 1: time budget of the sharded extra measurements")
     ap.add_argument("--no-seed-shard", action="store_true",
@@ -307,6 +310,10 @@ def main():
     frames = [synth.make_frame(args.config, 10000 * (0 if sharded else rank) + i) for i in range(2 * B)]
     n, d = frames[0].n, frames[0].D
     pool = torch.from_numpy(np.stack([f.emb for f in frames])).to(dev).view(2, B, n, d)
+    euclid = args.metric == "euclid"
+    h_run = (2.0 * H) ** 0.5 if euclid else H
+    if euclid:  # unit rows: |x - s|^2 = 2 (1 - x.s) at the start, so the windows match cosine h
+        pool = pool / pool.norm(dim=-1, keepdim=True)
     labels = torch.empty((B, n), dtype=torch.int32, device=dev)
     cent = torch.empty((B, CAP, d), dtype=torch.float32, device=dev)
     ctx = fms.context(local)
@@ -316,12 +323,14 @@ def main():
     gauss = args.kernel_profile == "gauss"
     if gauss:
         ctx.set_option("kernel_profile", 1)
+    if euclid:
+        ctx.set_option("metric", 1)
     pol = fms.default_policy(**policy_kwargs(n))
     stream = torch.cuda.current_stream(dev)
 
     def step(k, profile=False):
         rc, K, fs, rs = ctx.cluster_batch_ptr(pool[k % 2].data_ptr(), B, n, d, labels.data_ptr(), cent.data_ptr(),
-                                              CAP, H, MAX_ITERS, None, pol, stream.cuda_stream)
+                                              CAP, h_run, MAX_ITERS, None, pol, stream.cuda_stream)
         return fs, rs
 
     for k in range(args.warmup):
@@ -355,10 +364,10 @@ def main():
     # end-to-end through the host-pointer C-ABI entry (H2D + cluster + D2H inside the call)
     e2e = None
     if not args.no_e2e:
-        eh = torch.from_numpy(np.stack([f.emb for f in frames[:B]])).pin_memory()
+        eh = pool[0].cpu().pin_memory()  # the first input batch (row-normalised for --metric euclid)
         lh = torch.empty((B, n), dtype=torch.int32).pin_memory()
         ch = torch.empty((B, CAP, d), dtype=torch.float32).pin_memory()
-        ctx.cluster_host(eh, lh, ch, CAP, H, MAX_ITERS, None, pol, stream.cuda_stream)
+        ctx.cluster_host(eh, lh, ch, CAP, h_run, MAX_ITERS, None, pol, stream.cuda_stream)
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
@@ -366,7 +375,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(ksteps):
-            ctx.cluster_host(eh, lh, ch, CAP, H, MAX_ITERS, None, pol, stream.cuda_stream)
+            ctx.cluster_host(eh, lh, ch, CAP, h_run, MAX_ITERS, None, pol, stream.cuda_stream)
         e1.record(stream)
         torch.cuda.synchronize()
         ems = reduce_max(e0.elapsed_time(e1), world, dev)
@@ -379,7 +388,8 @@ def main():
     flops = totals["iter_seed_iters"] * n * 4 * d + totals["iter_count_units"] * n * 2 * d
     achieved = flops / (totals["iter_ms"] / 1e3) / 1e12 if totals["iter_ms"] > 0 else None
     peak = peaks["bf16_tflops_sustained"]
-    roof = {"bound": "tensor", "kernel": "fms::iter_kernel<16> (K2)", "achieved": achieved, "peak": peak,
+    dp = 16 if d + (2 if euclid else 0) <= 16 else 32  # operand row width of the K2 instantiation
+    roof = {"bound": "tensor", "kernel": f"fms::iter_kernel<{dp}, false> (K2)", "achieved": achieved, "peak": peak,
             "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(),
             "peak_source": f"{src} bf16 dense sustained (fp16 = bf16 rate); burst {peaks['bf16_tflops']}",
             "flops_per_launch": flops / max(1, totals["iter_launches"]),
@@ -413,7 +423,7 @@ def main():
             roof_terms["bound"] = "sfu"
             roof_terms["frac"] = sfu_ms / ms if ms > 0 else None
         ach = exps / (totals["iter_ms"] / 1e3) / 1e9 if totals["iter_ms"] > 0 else None
-        roof = {"bound": "sfu", "kernel": "fms::iter_kernel<16, true> (K2, Gaussian profile)", "achieved": ach,
+        roof = {"bound": "sfu", "kernel": f"fms::iter_kernel<{dp}, true> (K2, Gaussian profile)", "achieved": ach,
                 "peak": sfu_peak, "unit": "Gexp2/s", "frac": (ach / sfu_peak) if ach else None, "traffic": None,
                 "peak_source": "derived: 148 SMs x 16 MUFU.EX2/clk/SM x sm_max_mhz",
                 "tensor_achieved_tflops": achieved, "tensor_peak_tflops": peak,
@@ -431,7 +441,8 @@ def main():
         "dtype": "f16x3 split / f32 accumulate", "data": "synthetic",
         "config": {"workload": f"{args.config}: {f0.H}x{f0.W} frame, {d}-D, {f0.cells} touching/overlapping cells "
                                f"+ background, full OSOP (N_initial 128, gamma 0.9, L 2, P 0.99)"
-                               + (", Gaussian kernel profile (NEXT-4)" if gauss else ""),
+                               + (", Gaussian kernel profile (NEXT-4)" if gauss else "")
+                               + (", Euclidean metric, rows normalised, h = sqrt(0.2) (NEXT-4)" if euclid else ""),
                    "frames_per_step": B, "l2": "2 alternating input batches of B x 16 MiB (> 126 MB L2)",
                    "parallelism": f"seed-sharded x{world} ({args.backend})" if sharded else f"replicas x{world}"},
         "roofline": roof,
