@@ -347,15 +347,28 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
       tc_fence_after();
       const uint32_t gq = tmem + lane_base + Cfg::G_COL + ab * Cfg::G_N;
       if (w.mode == 0) {
-        uint32_t g[2 * DP];
-        tmem_ld32(gq, *reinterpret_cast<uint32_t(*)[32]>(g));
-        if constexpr (DP == 32) tmem_ld32(gq + 32, *reinterpret_cast<uint32_t(*)[32]>(g + 32));
-        tmem_ld_wait();
-        tmem_regs_ready(*reinterpret_cast<uint32_t(*)[32]>(g));
-        if constexpr (DP == 32) tmem_regs_ready(*reinterpret_cast<uint32_t(*)[32]>(g + 32));
+        if constexpr (DP == 16) {
+          uint32_t g[2 * DP];
+          tmem_ld32(gq, *reinterpret_cast<uint32_t(*)[32]>(g));
+          tmem_ld_wait();
+          tmem_regs_ready(*reinterpret_cast<uint32_t(*)[32]>(g));
 #pragma unroll
-        for (int k = 0; k < DP; ++k)
-          gs[k * kBM] += (double)__uint_as_float(g[k]) + (double)__uint_as_float(g[DP + k]) * (1.0 / kLimb);
+          for (int k = 0; k < DP; ++k)
+            gs[k * kBM] += (double)__uint_as_float(g[k]) + (double)__uint_as_float(g[DP + k]) * (1.0 / kLimb);
+        } else {
+          // DP = 32: the hi and lo halves one after the other (32 live registers instead of 64; the
+          // fp64 segment sums are exact either way)
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+            uint32_t g[32];
+            tmem_ld32(gq + part * 32, g);
+            tmem_ld_wait();
+            tmem_regs_ready(g);
+            const double sc = part ? 1.0 / kLimb : 1.0;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) gs[k * kBM] += (double)__uint_as_float(g[k]) * sc;
+          }
+        }
       }
       tc_fence_before();
       __syncwarp();
