@@ -241,7 +241,7 @@ def session(frames, h: float = 0.1, max_iter: int = 300, tol: float | None = Non
     out, Ns = [], []
     for emb in frames:
         p = policy(pol.kind, N, pol.gamma, pol.L, pol.H, pol.P, pol.has_background, pol.min_instance_px,
-                   pol.saturation_stop, pol.max_rounds, pol.rng_seed)
+                   pol.saturation_stop, pol.max_rounds, pol.rng_seed, pol.profile, pol.metric)
         r = cluster(emb, h=h, max_iter=max_iter, tol=tol, pol=p, centres_cap=centres_cap)
         out.append(r)
         Ns.append(N)
