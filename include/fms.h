@@ -183,8 +183,9 @@ fms_status fms_cluster_batch(void* ctx, const float* emb, int32_t B, int64_t n, 
                              fms_run_stats* run_stats, void* stream);
 
 /* Same as fms_cluster_batch with HOST buffers: the embeddings are copied to the device, and labels /
- * centres copied back, inside the call (end-to-end entry).  The batch runs in chunks of option
- * "host_chunk" frames (default 32) through double-buffered device staging: a copy stream uploads
+ * centres copied back, inside the call (end-to-end entry).  The batch runs in chunks through
+ * double-buffered device staging -- a first chunk of host_chunk / 4 frames (option "host_chunk",
+ * default 48), then the rest split evenly into chunks of at most host_chunk: a copy stream uploads
  * chunk i+1 and downloads chunk i-1's results while chunk i is clustered (frames are independent, so
  * the results equal one fms_cluster_batch over all B frames).  Pinned host memory is needed for the
  * copies to overlap.  run_stats sums the chunks' counters. */

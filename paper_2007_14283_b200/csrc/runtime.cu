@@ -98,7 +98,7 @@ struct Ctx {
   int kprofile = 0;  // "kernel_profile": 0 flat (the paper), 1 Gaussian (NEXT-4)
   int metric = 0;    // "metric": 0 cosine (the paper's path), 1 Euclidean (NEXT-4)
   // host-buffer entry: chunked, double-buffered staging on a copy stream ("host_chunk")
-  int host_chunk = 32;
+  int host_chunk = 48;
   cudaStream_t cstream = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr}, ev_done = nullptr;
 };
@@ -755,8 +755,15 @@ fms_status fms_cluster_batch_host(void* ctx, const float* emb_host, int32_t B, i
   // The batch runs in chunks of up to host_chunk frames with double-buffered staging: the copy
   // stream uploads chunk i+1 (and downloads chunk i-1's results) while chunk i is clustered, so the
   // PCIe transfers overlap the compute (frames are independent, so chunking changes no result).
+  // chunk sizes: the first chunk is a quarter of host_chunk (its upload is the one transfer the
+  // compute cannot hide), the rest split evenly in chunks of at most host_chunk frames
   const int32_t chunk = std::max(1, std::min<int32_t>(B, c->host_chunk));
-  const int nchunks = (B + chunk - 1) / chunk;
+  std::vector<int32_t> c_off{0};
+  const int32_t first = B > chunk ? std::max<int32_t>(1, chunk / 4) : B;
+  c_off.push_back(first);
+  const int32_t rest = B - first, n_rest = (rest + chunk - 1) / chunk;  // the rest in even chunks
+  for (int32_t r = 1; r <= n_rest; ++r) c_off.push_back(first + (int32_t)((int64_t)rest * r / n_rest));
+  const int nchunks = (int)c_off.size() - 1;
   const int nbuf = nchunks > 1 ? 2 : 1;
   const size_t eb = align_up((size_t)chunk * n * d * 4, 1024);
   const size_t lb = align_up((size_t)chunk * n * 4, 1024);
@@ -782,9 +789,9 @@ fms_status fms_cluster_batch_host(void* ctx, const float* emb_host, int32_t B, i
   }
   cudaStream_t cs = c->cstream;
   auto buf = [&](int i) { return reinterpret_cast<uint8_t*>(c->stage) + (size_t)(i % nbuf) * per; };
-  auto rows = [&](int i) { return std::min<int32_t>(chunk, B - i * chunk); };
+  auto rows = [&](int i) { return c_off[i + 1] - c_off[i]; };
   auto h2d = [&](int i) -> cudaError_t {
-    const cudaError_t e = cudaMemcpyAsync(buf(i), emb_host + (size_t)i * chunk * n * d, (size_t)rows(i) * n * d * 4,
+    const cudaError_t e = cudaMemcpyAsync(buf(i), emb_host + (size_t)c_off[i] * n * d, (size_t)rows(i) * n * d * 4,
                                           cudaMemcpyHostToDevice, cs);
     return e != cudaSuccess ? e : cudaEventRecord(c->ev_in[i % nbuf], cs);
   };
@@ -809,7 +816,7 @@ fms_status fms_cluster_batch_host(void* ctx, const float* emb_host, int32_t B, i
     if (centres_cap > 0) CU(cudaMemsetAsync(d_cen, 0, (size_t)Bi * centres_cap * d * 4, st));
     fms_run_stats rs{};
     fms_status s = run_batch(c, d_emb, Bi, n, d, bandwidth, max_iters, tol, policy, d_lab, d_cen, centres_cap,
-                             K_out + (size_t)i * chunk, frame_stats ? frame_stats + (size_t)i * chunk : nullptr,
+                             K_out + c_off[i], frame_stats ? frame_stats + c_off[i] : nullptr,
                              &rs, st);
     if (s != FMS_OK && s != FMS_E_CAPACITY) {
       cudaStreamSynchronize(cs);
@@ -827,9 +834,9 @@ fms_status fms_cluster_batch_host(void* ctx, const float* emb_host, int32_t B, i
     acc.iter_count_units += rs.iter_count_units;
     CU(cudaEventRecord(c->ev_done, st));
     CU(cudaStreamWaitEvent(cs, c->ev_done, 0));
-    CU(cudaMemcpyAsync(labels_host + (size_t)i * chunk * n, d_lab, (size_t)Bi * n * 4, cudaMemcpyDeviceToHost, cs));
+    CU(cudaMemcpyAsync(labels_host + (size_t)c_off[i] * n, d_lab, (size_t)Bi * n * 4, cudaMemcpyDeviceToHost, cs));
     if (centres_cap > 0)
-      CU(cudaMemcpyAsync(centres_host + (size_t)i * chunk * centres_cap * d, d_cen, (size_t)Bi * centres_cap * d * 4,
+      CU(cudaMemcpyAsync(centres_host + (size_t)c_off[i] * centres_cap * d, d_cen, (size_t)Bi * centres_cap * d * 4,
                          cudaMemcpyDeviceToHost, cs));
     CU(cudaEventRecord(c->ev_out[i % nbuf], cs));
   }
