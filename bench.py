@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--metric", default="cosine", choices=["cosine", "euclid"],
                     help="euclid (NEXT-4, reading R24): the C2 frames row-normalised, Euclidean window "
                          "sqrt(2h) (the same windows as cosine h at the start), window-mean update")
+    ap.add_argument("--host-chunk", type=int, default=0, help="e2e: frames per host-entry chunk (0 = library default)")
     ap.add_argument("--extras-budget-s", type=float, default=300.0,
                     help="N > 1: time budget of the sharded extra measurements")
     ap.add_argument("--no-seed-shard", action="store_true",
@@ -325,6 +326,8 @@ def main():
         ctx.set_option("kernel_profile", 1)
     if euclid:
         ctx.set_option("metric", 1)
+    if args.host_chunk > 0:
+        ctx.set_option("host_chunk", args.host_chunk)
     pol = fms.default_policy(**policy_kwargs(n))
     stream = torch.cuda.current_stream(dev)
 
