@@ -147,16 +147,7 @@ class Context:
         the int32 device buffer by its sum over all ranks, ordered on the given stream, and return 0;
         world = 1 (fn None) turns sharding off.  paper_2007_14283_b200.dist builds fn from
         torch.distributed."""
-        if fn is None:
-            self._xfn = EXCHANGE_FN()
-        else:
-            def _cb(user, buf, count, stream, _fn=fn):
-                try:
-                    return int(_fn(buf, count, stream or 0))
-                except Exception as e:  # a Python exception must not unwind through the C library
-                    self._xerr = e
-                    return 1
-            self._xfn = EXCHANGE_FN(_cb)  # kept alive with the context
+        self._xfn = self._wrap_exchange(fn)  # kept alive with the context
         self._check(lib().fms_set_exchange(self.h, self._xfn, None, int(rank), int(world)))
 
     def _wrap_exchange(self, fn):
