@@ -108,6 +108,12 @@ def lib():
                                    P(np.float64, flags="C"), C.c_int32, C.POINTER(C.c_int32),
                                    C.POINTER(Trace)]
         L.fmso_num_threads.restype = C.c_int
+        L.fmso_observe.restype = C.c_int64
+        L.fmso_observe.argtypes = [P(np.int64, flags="C"), C.c_int64, C.c_int64, C.c_int32, C.c_int32,
+                                   C.POINTER(C.c_int32), C.POINTER(C.c_double)]
+        L.fmso_osop_stop.restype = C.c_int
+        L.fmso_osop_stop.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int64,
+                                     C.c_double, C.c_int32, C.c_int32, C.c_int32]
         _lib = L
     return _lib
 
@@ -250,6 +256,25 @@ def session(frames, h: float = 0.1, max_iter: int = 300, tol: float | None = Non
         nm = r.trace["round_nmin"][-1] if r.trace["rounds"] > 0 else -1.0
         N = max(1, session_next(r.trace["seeds_total"], nm, pol.H))
     return out, Ns
+
+
+def observe(hist, n: int, has_background: int = 1, min_instance_px: int = 0):
+    """OSOP observation (R14, R22): returns (background index or -1, I, r)."""
+    hist = np.ascontiguousarray(hist, dtype=np.int64)
+    I = C.c_int32(0)
+    r = C.c_double(0.0)
+    bg = lib().fmso_observe(hist if hist.size else np.zeros(1, np.int64), hist.size, int(n), int(has_background),
+                            int(min_instance_px), C.byref(I), C.byref(r))
+    return int(bg), I.value, r.value
+
+
+NMIN_INF = 2 ** 63 - 1
+
+
+def osop_stop(ncand: int, total: int, n: int, round_: int, max_rounds: int, nmin: int, L: float,
+              saturation_stop: int, I: int, I_prev: int) -> bool:
+    """OSOP stop rule after a round (R13, R22); nmin = NMIN_INF is infinite."""
+    return bool(lib().fmso_osop_stop(ncand, total, n, round_, max_rounds, nmin, L, saturation_stop, I, I_prev))
 
 
 def key(rng_seed: int, round_: int, i: int) -> int:

@@ -378,6 +378,42 @@ void fmso_assign_m(const double* x, int64_t n, int32_t d, const double* centres,
 }
 
 /* ---------------------------------------------------------------------------------------------
+ * OSOP observation ("I and r are calculated from the predicted segmentation"; SPEC S:263-270
+ * estimate_observation).  hist[k] = #pixels labelled k.  With has_background the largest cluster
+ * (lowest k on ties) is the background (R14); I = #clusters other than the background with at least
+ * min_instance_px pixels (R22; 0 = every cluster counts); r = 1 - |background| / n (the foreground
+ * ratio of Eq. 13), or r = 1 without a background.  Returns the background index (-1 if none).
+ * ------------------------------------------------------------------------------------------- */
+int64_t fmso_observe(const int64_t* hist, int64_t K, int64_t n, int32_t has_background, int32_t min_instance_px,
+                     int32_t* I_out, double* r_out) {
+  int64_t bg = -1;
+  if (has_background && K > 0) {
+    bg = 0;
+    for (int64_t k = 1; k < K; ++k)
+      if (hist[k] > hist[bg]) bg = k;
+  }
+  int32_t I = 0;
+  for (int64_t k = 0; k < K; ++k)
+    if (k != bg && hist[k] >= min_instance_px) ++I;
+  if (I_out) *I_out = I;
+  if (r_out) *r_out = bg >= 0 ? 1.0 - (double)hist[bg] / (double)n : 1.0;
+  return bg;
+}
+
+/* OSOP stop rule after round `round` (P:318 + R13, R22): stop when no uncovered unvisited pixel
+ * remains (ncand == 0), every pixel has been a seed (total >= n), the round cap is reached, the seeds
+ * used so far reach L * N_min (Eq. 21's lower bound; nmin = INT64_MAX is infinite), or -- with
+ * saturation_stop -- the round did not raise the observed instance count (I <= I_prev, round >= 1).
+ * Returns 1 to stop, 0 to run another round with "N doubled" (K_next = min(total, ncand)). */
+int fmso_osop_stop(int64_t ncand, int64_t total, int64_t n, int32_t round, int32_t max_rounds, int64_t nmin,
+                   double L, int32_t saturation_stop, int32_t I, int32_t I_prev) {
+  if (ncand == 0 || total >= n || round + 1 >= max_rounds) return 1;
+  if (nmin != INT64_MAX && (double)total >= L * (double)nmin) return 1;
+  if (saturation_stop && round >= 1 && I <= I_prev) return 1;
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------------------------
  * The whole method: Alg. 2 wrapped in the OSOP controller of Fig. 3 / P:316-318.
  *   round 0: K_0 = N_initial (OSOP), n_seeds (FIXED) or n (ALL = Alg. 1, gamma = 1)
  *   each round: select -> lockstep mean-shift -> merge with previous centres -> assign all pixels
@@ -512,23 +548,15 @@ int fmso_cluster(const float* emb, int64_t n, int32_t d, double h, int32_t max_i
     if (pol->kind != FMSO_SEEDS_OSOP) break;
 
     /* OSOP (Eq. 12-19) */
-    int64_t bg = -1;
-    if (pol->has_background) {
-      bg = 0;
-      for (int64_t k = 1; k < Kc; ++k)
-        if (hist[k] > hist[bg]) bg = k;
-    }
     int32_t I = 0;
-    for (int64_t k = 0; k < Kc; ++k)
-      if (k != bg && hist[k] >= pol->min_instance_px) ++I;
-    double r = bg >= 0 ? 1.0 - (double)hist[bg] / (double)n : 1.0;
+    double r = 1.0;
+    fmso_observe(hist, Kc, n, pol->has_background, pol->min_instance_px, &I, &r);
     int64_t nmin = fmso_n_min(pol->P, I, r);
     tr.round_I[round] = I;
     tr.round_r[round] = r;
     tr.round_nmin[round] = nmin == INT64_MAX ? -1.0 : (double)nmin;
-    int stop = ncand2 == 0 || total >= n || round + 1 >= pol->max_rounds ||
-               (nmin != INT64_MAX && (double)total >= pol->L * (double)nmin) ||
-               (pol->saturation_stop && round >= 1 && I <= I_prev);
+    int stop = fmso_osop_stop(ncand2, total, n, round, pol->max_rounds, nmin, pol->L, pol->saturation_stop, I,
+                              I_prev);
     I_prev = I;
     if (stop) break;
     K_next = total < ncand2 ? total : ncand2;

@@ -65,6 +65,15 @@ int32_t fmso_need(double gamma, int64_t K);                  /* ceil(gamma*K) (R
  * nmin < 0 means N_min = infinity (no instance observed): N_next = total. */
 int64_t fmso_session_next(int64_t total, double nmin, double H);
 
+/* OSOP observation of the segmentation (R14, R22): background = the largest
+ * cluster (lowest index on ties) when has_background; I = other clusters with >= min_instance_px
+ * pixels; r = 1 - |bg|/n (1 without background).  Returns the background index or -1. */
+int64_t fmso_observe(const int64_t* hist, int64_t K, int64_t n, int32_t has_background, int32_t min_instance_px,
+                     int32_t* I_out, double* r_out);
+/* OSOP stop rule (R13, R22): 1 = stop, 0 = another round.  nmin = INT64_MAX is infinite. */
+int fmso_osop_stop(int64_t ncand, int64_t total, int64_t n, int32_t round, int32_t max_rounds, int64_t nmin,
+                   double L, int32_t saturation_stop, int32_t I, int32_t I_prev);
+
 /* ---- vector pieces ---- */
 int fmso_normalize(const float* emb, int64_t n, int32_t d, double* xhat);         /* Eq. 1 / 9 */
 int64_t fmso_select(const uint8_t* cand, int64_t n, int64_t K, uint64_t rng_seed,

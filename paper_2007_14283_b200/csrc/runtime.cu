@@ -330,12 +330,6 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
     if (bytes > c->pbuf_bytes) {
       CU(cudaStreamSynchronize(st));
       if (c->pbuf) cudaFree(c->pbuf);
-  for (int i = 0; i < 2; ++i) {
-    if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
-    if (c->ev_out[i]) cudaEventDestroy(c->ev_out[i]);
-  }
-  if (c->ev_done) cudaEventDestroy(c->ev_done);
-  if (c->cstream) cudaStreamDestroy(c->cstream);
       c->pbuf = nullptr;
       c->pbuf_bytes = 0;
       if (cudaMalloc(&c->pbuf, bytes) != cudaSuccess) {
