@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--config", default=CONFIG)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0,
+                    help="cpu_baseline: seconds of oracle work per thread setting (nproc, then 1 thread)")
     ap.add_argument("--shard", default="replicas", choices=["replicas", "seeds"],
                     help="replicas: every rank clusters its own frames (weak scaling); seeds: every rank "
                          "clusters the same frames and iterates 1/N of each round's seeds (strong scaling, "
@@ -157,21 +159,132 @@ def ncu_traffic():
         return None
 
 
-def cpu_baseline(frames, budget_s=20.0):
-    """The oracle as it stands, on a bounded sample of the same workload (rank 0, N=1 only)."""
-    import oracle
-    pk = policy_kwargs(frames[0].n)
-    done, t0 = 0, time.perf_counter()
-    for f in frames:
-        r = oracle.cluster(f.emb, h=H, max_iter=MAX_ITERS, pol=oracle.policy(rng_seed=f.seed, **pk))
-        assert r.status == 0
-        done += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": "frames/s", "cores": oracle.lib().fmso_num_threads(), "kind": "oracle",
-            "sample": f"{done} {frames[0].config} frame(s) ({frames[0].H}x{frames[0].W}x{frames[0].D}), "
-                      f"fp64 C oracle with OpenMP, {dt:.1f} s"}
+_CPU_CODE = r"""
+import json, sys, time
+sys.path.insert(0, sys.argv[1])
+import oracle, synth
+from synth.frames import min_instance_px
+cfg, first, budget, h, max_iter = sys.argv[2], int(sys.argv[3]), float(sys.argv[4]), float(sys.argv[5]), int(sys.argv[6])
+done, sit, t0, i = 0, 0, time.perf_counter(), first
+while True:
+    f = synth.make_frame(cfg, i)
+    r = oracle.cluster(f.emb, h=h, max_iter=max_iter,
+                       pol=oracle.policy(rng_seed=0, min_instance_px=min_instance_px(f.n), saturation_stop=1))
+    assert r.status == 0
+    done += 1
+    sit += r.trace["seed_iters"]
+    i += 1
+    if time.perf_counter() - t0 > budget:
+        break
+print(json.dumps({"frames": done, "seconds": time.perf_counter() - t0, "seed_iters": sit,
+                  "threads": oracle.lib().fmso_num_threads(), "seeds": [first, i - 1]}))
+"""
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_run(config, first, budget_s, threads):
+    """The oracle as it stands (plain C, fp64, OpenMP over seeds/pixels) in a child process with
+    OMP_NUM_THREADS=threads on frames first, first+1, ... of the GPU arm's own pool (the same
+    generator seeds) until budget_s is spent (at least one frame)."""
+    env = dict(os.environ, OMP_NUM_THREADS=str(threads))
+    p = subprocess.run([sys.executable, "-c", _CPU_CODE, ROOT, config, str(first), str(budget_s), str(H),
+                        str(MAX_ITERS)], capture_output=True, text=True, env=env, timeout=budget_s * 20 + 600)
+    return json.loads(p.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline(config, budget_s=20.0, first=0):
+    """cpu_baseline of the JSON line (rank 0, N = 1): the oracle on the host cores at nproc threads
+    and at 1 thread, each on a bounded sample of the GPU arm's own frames (pool seeds 0, 1, ...).
+    Per-frame work varies several-fold between frames, so the seed-iterations per second (the
+    algorithmic work rate) are reported beside frames/s."""
+    nproc = os.cpu_count() or 1
+    full = cpu_run(config, first, budget_s, nproc)
+    one = cpu_run(config, first, budget_s, 1)
+    return {"value": full["frames"] / full["seconds"], "unit": "frames/s", "cores": full["threads"],
+            "kind": "oracle",
+            "sample": f"{config} frames of the GPU pool, generator seeds {full['seeds'][0]}..{full['seeds'][1]} "
+                      f"({full['frames']} frame(s), {full['seconds']:.1f} s), fp64 C oracle, OpenMP",
+            "seed_iters_per_s": full["seed_iters"] / full["seconds"],
+            "one_thread": {"value": one["frames"] / one["seconds"], "unit": "frames/s", "cores": 1,
+                           "seed_iters_per_s": one["seed_iters"] / one["seconds"],
+                           "sample": f"generator seeds {one['seeds'][0]}..{one['seeds'][1]} ({one['frames']} "
+                                     f"frame(s), {one['seconds']:.1f} s)"},
+            "cpu_model": cpu_model(), "nproc": nproc}
+
+
+def latency_and_b16(ctx, pool, pol, h_run, stream, reps=20):
+    """SURVEY 8(d) timing protocol extras (one GPU): single-frame latency (median / p90 over `reps`
+    calls, each frame a different pool frame) with the input resident and through the host-buffer
+    entry (H2D + D2H inside the call), and batched throughput at B = 16, both ways."""
+    import numpy as np
+    import torch
+    dev = pool.device
+    B2, n, d = pool.shape[1], pool.shape[2], pool.shape[3]
+    flat = pool.reshape(-1, n, d)
+    lab = torch.empty((16, n), dtype=torch.int32, device=dev)
+    cen = torch.empty((16, CAP, d), dtype=torch.float32, device=dev)
+    out = {}
+
+    def dev_call(x, Bx):
+        ctx.cluster_batch_ptr(x.data_ptr(), Bx, n, d, lab.data_ptr(), cen.data_ptr(), CAP, h_run, MAX_ITERS, None,
+                              pol, stream.cuda_stream)
+
+    lat = []
+    for r in range(reps + 2):
+        x = flat[r % flat.shape[0]]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dev_call(x, 1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if r >= 2:
+            lat.append(e0.elapsed_time(e1))
+    eh = flat[:16].cpu().pin_memory()
+    lh = torch.empty((16, n), dtype=torch.int32).pin_memory()
+    ch = torch.empty((16, CAP, d), dtype=torch.float32).pin_memory()
+    lat_h = []
+    for r in range(reps + 2):
+        t0 = time.perf_counter()
+        ctx.cluster_host(eh[r % 16:r % 16 + 1], lh[:1], ch[:1], CAP, h_run, MAX_ITERS, None, pol, stream.cuda_stream)
+        torch.cuda.synchronize()
+        if r >= 2:
+            lat_h.append((time.perf_counter() - t0) * 1e3)
+    q = lambda v, p: float(np.percentile(np.array(v), p))  # noqa: E731
+    out["latency_ms"] = {"median": q(lat, 50), "p90": q(lat, 90), "calls": reps,
+                         "entry": "fms_cluster_batch, B = 1, input resident (CUDA events)"}
+    out["latency_e2e_ms"] = {"median": q(lat_h, 50), "p90": q(lat_h, 90), "calls": reps,
+                             "entry": "fms_cluster_batch_host, B = 1, pinned host buffers (host wall clock)"}
+    # B = 16 throughput: 5 steps over two alternating 16-frame batches
+    x16 = [flat[:16], flat[16:32] if flat.shape[0] >= 32 else flat[:16]]
+    dev_call(x16[0], 16)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(5):
+        dev_call(x16[k % 2], 16)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    out["b16"] = {"value": 80 / (e0.elapsed_time(e1) / 1e3), "unit": "frames/s", "steps": 5, "frames_per_step": 16}
+    ctx.cluster_host(eh, lh, ch, CAP, h_run, MAX_ITERS, None, pol, stream.cuda_stream)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for k in range(5):
+        ctx.cluster_host(eh, lh, ch, CAP, h_run, MAX_ITERS, None, pol, stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    out["b16_e2e"] = {"value": 80 / (e0.elapsed_time(e1) / 1e3), "unit": "frames/s", "steps": 5,
+                      "h2d_bytes_per_step": 16 * n * d * 4, "d2h_bytes_per_step": 16 * n * 4 + 16 * CAP * d * 4}
+    return out
 
 
 def seed_sharded_c4(world, rank, local, B=2, warmup=1, steps=3):
@@ -271,13 +384,18 @@ def run_reference(args, world, rank):
     if rank != 0:  # the reference arm runs on rank 0 only; other ranks exit 0 without work
         return
     import synth
-    frames = [synth.make_frame(args.config, 1000 + i) for i in range(max(1, args.steps + args.warmup))]
-    for f in frames[:args.warmup]:
-        cpu_baseline([f], budget_s=0)
+    f0 = synth.make_frame(args.config, 0)
+    # each step clusters one frame of the GPU arm's pool (generator seeds 0, 1, ...), warm-up first
+    if args.warmup > 0:
+        cpu_run(args.config, 0, 0.0, os.cpu_count() or 1)
     t0 = time.perf_counter()
-    cb = cpu_baseline(frames[args.warmup:args.warmup + args.steps], budget_s=1e9)
+    runs = [cpu_run(args.config, k, 0.0, os.cpu_count() or 1) for k in range(args.steps)]
     dt = time.perf_counter() - t0
-    f0 = frames[0]
+    frames_done = sum(r["frames"] for r in runs)
+    secs = sum(r["seconds"] for r in runs)
+    cb = {"value": frames_done / secs, "unit": "frames/s", "cores": runs[0]["threads"], "kind": "oracle",
+          "sample": f"{args.config} frames of the GPU pool, generator seeds 0..{args.steps - 1}, one per step",
+          "seed_iters_per_s": sum(r["seed_iters"] for r in runs) / secs, "cpu_model": cpu_model()}
     # the fms arm's metric and workload strings (same config); each step is a bounded sample of it
     line = {"impl": "reference",
             "metric": f"frames/sec ({f0.H}x{f0.W}, {f0.D}-D embeddings) and mean-shift iteration % of roofline",
@@ -341,21 +459,17 @@ def main():
 
     for k in range(args.warmup):
         step(k)
-    ctx.set_option("profile_iter", 1)
     totals = dict(iter_ms=0.0, iter_seed_iters=0, iter_count_units=0, iter_launches=0, launches=0, frames=0,
                   seed_iters=0, assign_pairs=0)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    # the headline: K steps, no per-kernel instrumentation inside the timed region
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for k in range(args.steps):
             fs, rs = step(k)
-            totals["iter_ms"] += rs["iter_ms"]
-            totals["iter_seed_iters"] += rs["iter_seed_iters"]
-            totals["iter_count_units"] += rs["iter_count_units"]
-            totals["iter_launches"] += rs["iter_launches"]
             totals["launches"] += rs["launches"]
             totals["frames"] += B
             totals["seed_iters"] += sum(f["seed_iters"] for f in fs)
@@ -363,9 +477,24 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = reduce_max(ev0.elapsed_time(ev1), world, dev)
-    ctx.set_option("profile_iter", 0)
     frames_total = totals["frames"] * (1 if sharded else world)
     value = frames_total / (ms / 1e3)
+    # a separate profiled pass for the roofline: CUDA events around every K2 launch on the work stream
+    prof_steps = max(1, min(args.steps, 6))
+    ctx.set_option("profile_iter", 1)
+    prof_ms_total = 0.0
+    for k in range(prof_steps):
+        e0p, e1p = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0p.record(stream)
+        fs, rs = step(k)
+        e1p.record(stream)
+        torch.cuda.synchronize()
+        prof_ms_total += e0p.elapsed_time(e1p)
+        totals["iter_ms"] += rs["iter_ms"]
+        totals["iter_seed_iters"] += rs["iter_seed_iters"]
+        totals["iter_count_units"] += rs["iter_count_units"]
+        totals["iter_launches"] += rs["iter_launches"]
+    ctx.set_option("profile_iter", 0)
 
     # end-to-end through the host-pointer C-ABI entry (H2D + cluster + D2H inside the call)
     e2e = None
@@ -395,16 +524,20 @@ def main():
     achieved = flops / (totals["iter_ms"] / 1e3) / 1e12 if totals["iter_ms"] > 0 else None
     peak = peaks["bf16_tflops_sustained"]
     dp = 16 if d + (2 if euclid else 0) <= 16 else 32  # operand row width of the K2 instantiation
-    roof = {"bound": "tensor", "kernel": f"fms::iter_kernel<{dp}, false> (K2)", "achieved": achieved, "peak": peak,
+    roof = {"bound": "tensor", "kernel": f"fms::iter8_kernel<{dp}> (K2, int8 exact weighted sum)", "achieved": achieved,
+            "peak": peak,
             "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(),
             "peak_source": f"{src} bf16 dense sustained (fp16 = bf16 rate); burst {peaks['bf16_tflops']}",
             "flops_per_launch": flops / max(1, totals["iter_launches"]),
             "ms_per_launch": totals["iter_ms"] / max(1, totals["iter_launches"]),
-            "iter_share_of_step": totals["iter_ms"] / ms if ms > 0 else None}
-    # frame-level roofline: algorithmic iteration FLOPs of the whole job at the tensor peak
-    frame_roof_ms = flops / (peak * 1e12) * 1e3
+            "iter_share_of_step": totals["iter_ms"] / prof_ms_total if prof_ms_total > 0 else None,
+            "measured": f"separate profiled pass of {prof_steps} step(s) after the timed region"}
+    # frame-level roofline: algorithmic iteration FLOPs of the whole timed job at the tensor peak (the
+    # K2 launches' work of the timed steps: seed-iterations of every frame)
+    job_iter_flops = totals["seed_iters"] * n * 4 * d
+    frame_roof_ms = job_iter_flops / (peak * 1e12) * 1e3
     # + the assignment's contraction (2 n D per pixel-centre pair per round) for the job terms
-    job_flops = flops + totals["assign_pairs"] * n * 2 * d
+    job_flops = job_iter_flops + totals["assign_pairs"] * n * 2 * d
     job_tensor_ms = job_flops / (peak * 1e12) * 1e3
     # north_star / SURVEY 8(d): the job's roofline is the slowest of three limits -- contraction FLOPs
     # at the tensor peak, kernel exponentials at the SFU peak (0: the flat kernel has none, Eq. 3/11),
@@ -420,7 +553,7 @@ def main():
     # the iteration steps; peak = 148 SMs x 16 MUFU results/clk/SM x the max SM clock (DESIGN 6)
     clk_ghz = (peaks.get("sm_max_mhz") or 1965.0) / 1e3
     sfu_peak = 148 * 16 * clk_ghz  # G exp2/s
-    exps = totals["iter_seed_iters"] * n if gauss else 0
+    exps = totals["seed_iters"] * n if gauss else 0
     sfu_ms = exps / (sfu_peak * 1e9) * 1e3
     if gauss:
         roof_terms["sfu_ms"] = sfu_ms
@@ -428,16 +561,20 @@ def main():
         if sfu_ms > max(job_tensor_ms, hbm_ms):
             roof_terms["bound"] = "sfu"
             roof_terms["frac"] = sfu_ms / ms if ms > 0 else None
-        ach = exps / (totals["iter_ms"] / 1e3) / 1e9 if totals["iter_ms"] > 0 else None
+        ach = totals["iter_seed_iters"] * n / (totals["iter_ms"] / 1e3) / 1e9 if totals["iter_ms"] > 0 else None
         roof = {"bound": "sfu", "kernel": f"fms::iter_kernel<{dp}, true> (K2, Gaussian profile)", "achieved": ach,
                 "peak": sfu_peak, "unit": "Gexp2/s", "frac": (ach / sfu_peak) if ach else None, "traffic": None,
                 "peak_source": "derived: 148 SMs x 16 MUFU.EX2/clk/SM x sm_max_mhz",
                 "tensor_achieved_tflops": achieved, "tensor_peak_tflops": peak,
                 "ms_per_launch": totals["iter_ms"] / max(1, totals["iter_launches"]),
-                "iter_share_of_step": totals["iter_ms"] / ms if ms > 0 else None}
+                "iter_share_of_step": totals["iter_ms"] / prof_ms_total if prof_ms_total > 0 else None}
+    extras = {}
+    if world == 1 and not sharded:
+        extras = latency_and_b16(ctx, pool, pol, h_run, stream)
     cb = None
     if world == 1 and not args.no_cpu:
-        cb = cpu_baseline([synth.make_frame(args.config, 20000 + i) for i in range(3)], budget_s=20.0)
+        cb = cpu_baseline(args.config, budget_s=args.cpu_budget_s)
+        cb["gpu_seed_iters_per_s"] = totals["seed_iters"] / (ms / 1e3)
     f0 = frames[0]
     line = {
         "metric": f"frames/sec ({f0.H}x{f0.W}, {d}-D embeddings) and mean-shift iteration % of roofline",
@@ -460,6 +597,7 @@ def main():
         "e2e": e2e,
         "cpu_baseline": cb,
     }
+    line.update(extras)
     if world > 1 and not sharded and not args.no_seed_shard:
         # strong-scaling extras (C4 seed-sharded, C5 pixel-sharded) after the headline measurement; a
         # watchdog prints the headline line and ends every rank if they overrun (a stuck collective

@@ -211,8 +211,25 @@ class Context:
                      max_iters: int = 300, tol: float | None = None, policy: Policy | None = None, stream: int = 0,
                      allow=()):
         """Host-buffer entry (end-to-end): emb_host [B,n,d] float32, labels_host [B,n] int32,
-        centres_host [B,cap,d] float32 -- all pinned CPU torch tensors (or anything with data_ptr())."""
+        centres_host [B,cap,d] float32 -- all contiguous CPU torch tensors (pinned for the copies to
+        overlap).  Shapes and dtypes are checked before the call: the library writes B*n labels and
+        B*centres_cap*d centre values through the raw pointers."""
+        import torch
+        for name, t, dt in (("emb_host", emb_host, torch.float32), ("labels_host", labels_host, torch.int32),
+                            ("centres_host", centres_host, torch.float32)):
+            if not isinstance(t, torch.Tensor):
+                raise TypeError(f"{name} must be a torch tensor")
+            if t.device.type != "cpu" or t.dtype != dt or not t.is_contiguous():
+                raise TypeError(f"{name} must be a contiguous CPU {dt} tensor")
+        if emb_host.dim() != 3:
+            raise ValueError("emb_host must be [B, n, d]")
         B, n, d = emb_host.shape
+        if tuple(labels_host.shape) != (B, n):
+            raise ValueError(f"labels_host must be [{B}, {n}], got {tuple(labels_host.shape)}")
+        if centres_cap < 0 or centres_host.dim() != 3 or centres_host.shape[0] != B or \
+                centres_host.shape[1] != centres_cap or centres_host.shape[2] != d:
+            raise ValueError(f"centres_host must be [{B}, centres_cap={centres_cap}, {d}], "
+                             f"got {tuple(centres_host.shape)}")
         tol = h / 1000.0 if tol is None else tol
         policy = policy if policy is not None else default_policy()
         K = (C.c_int32 * B)()

@@ -410,7 +410,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         // P[pb] is free once the weighted sum of the tile that used it last has completed: probe
         // now, use the answer after the flat kernel
         const uint32_t u = ctile - Cfg::NP;
-        const bool need_free = w.mode == 0 && ctile >= (uint32_t)Cfg::NP;
+        // (count-pass tiles too: p_full must not complete twice before MMA2 has seen the first phase)
+        const bool need_free = ctile >= (uint32_t)Cfg::NP;
         bool p_free = !need_free || mbar_test(&x_empty[u % Cfg::STAGES], (u / Cfg::STAGES) & 1);
         uint32_t pk[kColsPerWarp / 2];
         if (GAUSS && w.mode == 0) {  // count passes (intensity, R10) keep the flat window

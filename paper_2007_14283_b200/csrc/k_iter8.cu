@@ -1,0 +1,489 @@
+// k_iter8.cu -- K2 for the flat kernel (the paper's path): the lockstep mean-shift iteration with the
+// weighted sum as an exact 8-bit integer contraction on the 5th-generation tensor cores.
+//
+// One lockstep step of Alg. 2 lines 4-9 for every active seed of every frame,
+// evaluated densely as P:210 prescribes:
+//
+//     C = S_hat . X_hat^T              seeds x pixels cosine similarity   (Eq. 1/9)
+//     W = [C >= tau], tau = 1 - h      flat kernel, inclusive              (Eq. 11; R5)
+//     G = W . X_hat                    windowed sum (count cancels, R4)    (Eq. 8 / R1)
+//
+// Similarity: as in k_iter.cu, three kind::f16 MMAs over fixed-point fp16 limbs (s_hi.hi +
+// (s_hi 2^-11).lo + s_lo.hi, error ~1e-7) into an fp32 TMEM accumulator.
+//
+// Weighted sum: the pixels are also stored as int8 digit planes of v = round(2^22 x_hat) =
+// a 2^16 + b 2^8 + c (fms_device.cuh `digits`), 3 DP planes of 128 pixels per tile, K-major.  The
+// in-window weight is the byte 255 (unsigned), so
+//     Gq[:, j DP + k] = 255 sum_{in window} digit_j(x_k)        (kind::i8, s32 accumulate: EXACT)
+// and G_k = (Gq[a] 2^16 + Gq[b] 2^8 + Gq[c]) / 255 = sum_{in window} v_k, an integer.  Per tile that
+// is 4 MMAs of K = 32 pixels (the fp16 weighted sum needs 8 of K = 16), and the weights take 32
+// TMEM columns per tile instead of 64.  Integer sums are exact for any split of the pixels, so work
+// items are sized freely (plan_kernel) and CTAs merge with fp64 atomics of integers (order-free).
+//
+// Flat kernel in the epilogue: with C and tau_m (the float just below 2^11 tau) fp32,
+//     v = C - tau_m  has its sign bit clear and a nonzero value  <=>  C > tau_m  <=>  C >= 2^11 tau
+// (the rounded difference keeps the sign of the exact one and is zero only when C = tau_m).  FADD2
+// forms two differences per instruction; I2IP (cvt.pack.sat.u8.s32) saturates the float bits read as
+// int32 -- positive -> 255, zero or negative -> 0 -- and packs two pixels per instruction, chaining
+// the previous pair into the upper half.  Four pixels' weights cost 2 FADD2 + 2 I2IP.
+//
+// Structure (fused-attention style; the S x N weights never leave the SM):
+//   * work item = (frame, 128-seed tile, chunk of `ct` 128-pixel tiles; ct chosen per launch by
+//     plan_kernel).  Persistent CTAs (one per SM) take equal contiguous ranges of the item list.
+//   * warp 16  : TMA producer -- seed tile (s_hi, s_hi 2^-11, s_lo) and a ring of pixel tiles
+//                                (hi, lo limbs; digit planes).
+//   * warp 17  : MMA1 issuer  -- C[i % NC] = 3 MMAs (M=128, N=128, K=DP) into TMEM.
+//   * warp 18  : MMA2 issuer  -- Gq += P[i % NP] . Q (kind::i8, A = P from TMEM, N = 3 DP).
+//   * warps 0-15: epilogue    -- two groups of 8 warps take alternate tiles: one tcgen05.ld of 64
+//                                columns of C per warp, C handed back to MMA1, flat kernel -> u8
+//                                weights (tcgen05.st of 16 columns).  The group that handled an
+//                                item's last tile drains Gq into its own int64 segment sums.
+//                                Count-pass items (mode 1: the converged modes of a round) skip the
+//                                weighted sum and count window members (intensity, R10).
+//   TMEM: NC x 128 columns of C + NP x 32 columns of P + 3 DP columns of Gq.
+#include "fms_device.cuh"
+
+namespace fms {
+
+namespace k8 {
+constexpr int kEpiWarps = 16;
+constexpr int kWarpTma = kEpiWarps, kWarpMma1 = kEpiWarps + 1, kWarpMma2 = kEpiWarps + 2;
+constexpr int kThreads = (kEpiWarps + 3) * 32;
+}  // namespace k8
+
+template <int DP>
+struct Iter8Cfg {
+  // epilogue groups (tiles in flight): 4 groups of 4 warps for 16-lane rows; 32-lane rows keep 2
+  // groups of 8 (their segment sums and pixel stages would not fit shared memory with 4)
+#ifdef K8_GROUPS
+  static constexpr int GROUPS = DP == 16 ? K8_GROUPS : 2;
+#else
+  static constexpr int GROUPS = DP == 16 ? 4 : 2;
+#endif
+  static constexpr int GROUP_WARPS = k8::kEpiWarps / GROUPS;  // a multiple of 4 (one per lane quarter)
+  static constexpr int COLS_PER_WARP = kBN / (GROUP_WARPS / 4);
+  static constexpr int PARTS = COLS_PER_WARP / 64;            // 64-column tcgen05.ld per part
+  static constexpr int ROW_B = DP * 2;                    // bytes per fp16 row
+  static constexpr int TILE_B = kBN * ROW_B;              // one pixel tile (one limb)
+  static constexpr int A_B = kBM * ROW_B;                 // one seed tile (one split)
+  static constexpr uint32_t LAYOUT = DP == 16 ? 6u : 4u;  // SWIZZLE_32B / SWIZZLE_64B (fp16 rows)
+  static constexpr uint32_t SBO = 8 * ROW_B;              // 8-row core-matrix group stride
+  static constexpr int NQ = 3 * DP;                       // digit planes (= Gq columns)
+  static constexpr int Q_B = NQ * kBN;                    // digit planes of one tile (128 B rows, SW128)
+  static constexpr int STAGE_B = 2 * TILE_B + Q_B;
+#ifdef K8_NC
+  static constexpr int NC = K8_NC;
+#else
+  static constexpr int NC = DP == 16 ? 3 : 2;             // C buffers
+#endif
+  static constexpr int NP = DP == 16 ? (NC == 3 ? 2 : 3) : 3;  // P buffers (32 columns each)
+  static constexpr int P_COL = NC * kBN;
+  static constexpr int G_COL = P_COL + NP * (kBN / 4);
+  static_assert(G_COL + NQ <= 512, "TMEM budget");
+  static constexpr int STAGES = DP == 16 ? (GROUPS == 4 ? 9 : 11) : 4;
+  static constexpr int GS_B = kBM * DP * 8;               // int64 segment sums, [DP][kBM], per group
+  static constexpr int SMEM = 1024 + 6 * A_B + STAGES * STAGE_B + GROUPS * GS_B + 1024;
+  static_assert(SMEM <= 232448, "shared memory");
+  static_assert(STAGE_B % 1024 == 0 && (2 * TILE_B) % 1024 == 0, "SW128 alignment of the digit planes");
+};
+
+// chunk of pixel tiles per work item, chosen by plan_kernel for this launch
+struct Item8 {
+  int f, tile, chunk, mode, key;  // key: frame * S_pad + tile * kBM (the segment a G drain belongs to)
+};
+__device__ __forceinline__ Item8 item8(const Params& p, int item, int nch) {
+  const int t = item / nch;
+  const TileTask tt = p.tiles[t];
+  return Item8{tt.f, tt.tile, item - t * nch, tt.mode, tt.f * p.S_pad + tt.tile * kBM};
+}
+
+// two in-window differences per instruction: {c0 - tau_m, c1 - tau_m}
+__device__ __forceinline__ void sub_tau2(uint32_t c0, uint32_t c1, float tau_m, uint32_t& d0, uint32_t& d1) {
+  asm("{\n\t.reg .b64 ra, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rc, {%4, %4};\n\t"
+      "add.rn.f32x2 rd, ra, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=r"(d0), "=r"(d1)
+      : "r"(c0), "r"(c1), "f"(-tau_m));
+}
+// four pixels' weights, byte i = 255 if difference i > 0 else 0
+__device__ __forceinline__ uint32_t pack_w4(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3) {
+  uint32_t t, w;
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(t) : "r"(d3), "r"(d2));
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(w) : "r"(d1), "r"(d0), "r"(t));
+  return w;
+}
+
+// Timing experiment (tools/iter8_probe.cu): -DK8_TIMELINE logs clock64 events of CTA 0 into p.dbg,
+// [role][tile][event]; the production build compiles the hook away.
+// -DK8_OFF=bits switches parts off for timing: 1 MMA2, 2 MMA1, 4 C loads, 8 flat-kernel ALU,
+// 16 weight stores, 32 pixel TMA loads
+#ifdef K8_OFF
+#define K8_SKIP(bit) (K8_OFF & (bit))
+#else
+#define K8_SKIP(bit) (0)
+#endif
+#ifdef K8_TIMELINE
+#define K8_TL(role, tile, ev)                                                                  \
+  do {                                                                                         \
+    if (blockIdx.x == 0 && lane == 0 && (tile) < 512)                                          \
+      p.dbg[((size_t)(role) * 512 + (tile)) * 8 + (ev)] = clock64();                           \
+  } while (0)
+#else
+#define K8_TL(role, tile, ev) \
+  do {                        \
+  } while (0)
+#endif
+
+template <int DP>
+__global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_constant__ TMaps tm, Params p) {
+  using namespace k8;
+  using Cfg = Iter8Cfg<DP>;
+  constexpr int kGroups = Cfg::GROUPS, kGroupWarps = Cfg::GROUP_WARPS;
+  constexpr int kColsPerWarp = Cfg::COLS_PER_WARP, kParts = Cfg::PARTS;
+  const int n_items = p.counters[0];
+  const int ct = p.counters[12];   // pixel tiles per work item
+  const int nch = p.counters[13];  // work items per seed tile
+  const int i_begin = (int)(((long long)n_items * blockIdx.x) / gridDim.x);
+  const int i_end = (int)(((long long)n_items * (blockIdx.x + 1)) / gridDim.x);
+  if (i_begin >= i_end) return;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                                    // [2 buffers][s_hi, s_hs, s_lo][A_B]
+  uint8_t* sX = smem + 6 * Cfg::A_B;                     // [STAGES][hi, lo, digit planes]
+  long long* gsm = reinterpret_cast<long long*>(sX + Cfg::STAGES * Cfg::STAGE_B);  // [group][DP][kBM]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(gsm) + kGroups * Cfg::GS_B);
+  uint64_t* x_full = bars;                    // [STAGES] pixel tile landed
+  uint64_t* x_empty = x_full + Cfg::STAGES;   // [STAGES] tile's weighted sum done: stage and P free
+  uint64_t* a_full = x_empty + Cfg::STAGES;   // [2] seed tile landed
+  uint64_t* a_empty = a_full + 2;             // [2] seed tile consumed
+  // similarity ready: one barrier per epilogue GROUP (not per C buffer), so that a group never waits
+  // on a barrier whose previous phase is still pending (a waiter two phases ahead would see the
+  // pending phase's parity as complete)
+  uint64_t* c_full = a_empty + 2;             // [kGroups]
+  uint64_t* c_empty = c_full + kGroups;       // [NC] similarity loaded by the epilogue
+  // an item's Gq complete: per group -- the group owning the item's last tile drains it, and each
+  // group's drains are sequential in its own program order
+  uint64_t* g_full = c_empty + Cfg::NC;       // [kGroups]
+  uint64_t* g_empty = g_full + kGroups;       // [1] Gq drained
+  uint64_t* p_full = g_empty + 1;             // [NP] weights written
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(p_full + Cfg::NP);
+  static_assert((Cfg::STAGES * 2 + 5 + 2 * kGroups + Cfg::NC + Cfg::NP) * 8 + 4 <= 1024, "barrier area");
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < kGroups; ++i) mbar_init(&g_full[i], 1);
+    mbar_init(g_empty, 4);  // drained by 4 warps (one per lane quarter)
+    for (int i = 0; i < kGroups; ++i) mbar_init(&c_full[i], 1);
+    for (int i = 0; i < Cfg::NC; ++i) mbar_init(&c_empty[i], kGroupWarps);
+    for (int i = 0; i < Cfg::NP; ++i) mbar_init(&p_full[i], kGroupWarps);
+    fence_barrier_init();
+    fence_proxy_async();
+  }
+  if (warp == kWarpTma && lane == 0) {
+    tma_prefetch(&tm.xh); tma_prefetch(&tm.xl); tma_prefetch(&tm.xq);
+    tma_prefetch(&tm.sh); tma_prefetch(&tm.ss); tma_prefetch(&tm.sl);
+  }
+  if (warp == kWarpMma1) tmem_alloc(tmem_holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  if (warp == kWarpTma) {
+    // ================================ TMA producer ================================
+    int xi = 0;
+    int stage = 0;
+    uint32_t sphase = 0;
+    int it = 0;
+    for (int item = i_begin; item < i_end; ++item, ++it) {
+      const Item8 w = item8(p, item, nch);
+      const int ab = it & 1;
+      const int cbeg = w.chunk * ct;
+      const int ccnt = min(ct, p.n_ptiles - cbeg);
+      mbar_wait(&a_empty[ab], ((it >> 1) & 1) ^ 1);
+      if (lane == 0) {
+        const int srow = w.f * p.S_pad + w.tile * kBM;
+        mbar_expect_tx(&a_full[ab], 3 * Cfg::A_B);
+        tma_load_2d(sA + (3 * ab + 0) * Cfg::A_B, &tm.sh, &a_full[ab], 0, srow);
+        tma_load_2d(sA + (3 * ab + 1) * Cfg::A_B, &tm.ss, &a_full[ab], 0, srow);
+        tma_load_2d(sA + (3 * ab + 2) * Cfg::A_B, &tm.sl, &a_full[ab], 0, srow);
+      }
+      __syncwarp();
+      const long long tile0 = (long long)w.f * p.n_ptiles + cbeg;
+      for (int j = 0; j < ccnt; ++j) {
+        mbar_wait(&x_empty[stage], sphase ^ 1);
+        K8_TL(0, xi, 0);
+        if (lane == 0) {
+          uint8_t* st = sX + stage * Cfg::STAGE_B;
+          const int xrow = (int)((tile0 + j) * kBN);
+          if (K8_SKIP(32)) {
+            mbar_arrive(&x_full[stage]);
+          } else {
+            mbar_expect_tx(&x_full[stage], Cfg::STAGE_B);
+            tma_load_2d(st, &tm.xh, &x_full[stage], 0, xrow);
+            tma_load_2d(st + Cfg::TILE_B, &tm.xl, &x_full[stage], 0, xrow);
+            tma_load_2d(st + 2 * Cfg::TILE_B, &tm.xq, &x_full[stage], 0, (int)((tile0 + j) * Cfg::NQ));
+          }
+        }
+        __syncwarp();
+        ++xi;
+        if (++stage == Cfg::STAGES) { stage = 0; sphase ^= 1; }
+      }
+    }
+  } else if (warp == kWarpMma1) {
+    // ============================ MMA1 issuer: similarity ============================
+    constexpr uint32_t IDESC1 = idesc_f16(kBM, kBN, 0, 0);  // both operands K-major
+    const uint64_t dx0 = umma_desc(smem_u32(sX), 16, Cfg::SBO, Cfg::LAYOUT);
+    int stage = 0;
+    uint32_t sphase = 0;
+    int i = 0;
+    for (int item = i_begin, it = 0; item < i_end; ++item, ++it) {
+      const Item8 w = item8(p, item, nch);
+      const int ccnt = min(ct, p.n_ptiles - w.chunk * ct);
+      const int ab = it & 1;
+      mbar_wait(&a_full[ab], (it >> 1) & 1);
+      tc_fence_after();
+      const uint64_t dah = umma_desc(smem_u32(sA + (3 * ab + 0) * Cfg::A_B), 16, Cfg::SBO, Cfg::LAYOUT);
+      const uint64_t das = dah + (Cfg::A_B >> 4);
+      const uint64_t dal = dah + (2 * Cfg::A_B >> 4);
+      for (int j = 0; j < ccnt; ++j, ++i) {
+        const uint32_t buf = i % Cfg::NC;
+        K8_TL(1, i, 0);
+        if (i >= Cfg::NC) mbar_wait(&c_empty[buf], ((i / Cfg::NC) - 1) & 1);
+        K8_TL(1, i, 1);
+        mbar_wait(&x_full[stage], sphase);
+        K8_TL(1, i, 2);
+        tc_fence_after();
+        const uint64_t dxh = dx0 + (uint64_t)(stage * (Cfg::STAGE_B >> 4));
+        const uint64_t dxl = dxh + (Cfg::TILE_B >> 4);
+        const uint32_t d = tmem + buf * kBN;
+        if (!K8_SKIP(2)) {
+#pragma unroll
+          for (int kk = 0; kk < DP / 16; ++kk)  // s_hi . hi
+            mma_ss_f16_el(d, dah + kk * 2, dxh + kk * 2, IDESC1, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < DP / 16; ++kk)  // + (s_hi 2^-11) . lo
+            mma_ss_f16_el(d, das + kk * 2, dxl + kk * 2, IDESC1, 1u);
+#pragma unroll
+          for (int kk = 0; kk < DP / 16; ++kk)  // + s_lo . hi
+            mma_ss_f16_el(d, dal + kk * 2, dxh + kk * 2, IDESC1, 1u);
+        }
+        tc_commit_el(&c_full[i % kGroups]);
+        K8_TL(1, i, 3);
+        if (++stage == Cfg::STAGES) { stage = 0; sphase ^= 1; }
+      }
+      tc_commit_el(&a_empty[ab]);  // seed tile free once this item's MMA1s complete
+    }
+  } else if (warp == kWarpMma2) {
+    // ==================== MMA2 issuer: exact int8 weighted sum ====================
+    // Gq (+)= P[i % NP] . Q once the epilogue group has written the weights (p_full); one commit frees
+    // the pixel stage and with it the weight buffer (x_empty); at the end of an item hands Gq over.
+    constexpr uint32_t IDESC2 = idesc_i8(kBM, Cfg::NQ);
+    const uint64_t dq0 = umma_desc(smem_u32(sX + 2 * Cfg::TILE_B), 16, 1024, 2);  // K-major SW128
+    int stage = 0;
+    int i = 0;
+    const uint32_t g_tmem = tmem + Cfg::G_COL;
+    for (int item = i_begin, it = 0; item < i_end; ++item, ++it) {
+      const Item8 w = item8(p, item, nch);
+      const int ccnt = min(ct, p.n_ptiles - w.chunk * ct);
+      mbar_wait(g_empty, (it & 1) ^ 1);
+      tc_fence_after();
+      for (int j = 0; j < ccnt; ++j, ++i) {
+        const uint32_t pb = i % Cfg::NP;
+        K8_TL(2, i, 0);
+        mbar_wait(&p_full[pb], (i / Cfg::NP) & 1);
+        K8_TL(2, i, 1);
+        tc_fence_after();
+        if (w.mode == 0 && !K8_SKIP(1)) {
+          const uint64_t bq = dq0 + (uint64_t)(stage * (Cfg::STAGE_B >> 4));
+          const uint32_t pa = tmem + Cfg::P_COL + pb * (kBN / 4);
+#pragma unroll
+          for (int k = 0; k < kBN / 32; ++k)  // 32 pixels = 8 columns of packed u8 weights
+            mma_ts_i8_el(g_tmem, pa + k * 8, bq + (uint64_t)(k * 2), IDESC2, (j == 0 && k == 0) ? 0u : 1u);
+        }
+        tc_commit_el(&x_empty[stage]);  // pixel stage and weight buffer pb free once these complete
+        K8_TL(2, i, 2);
+        if (++stage == Cfg::STAGES) stage = 0;
+      }
+      tc_commit_el(&g_full[(i - 1) % kGroups]);  // the group that handled the item's last tile drains
+    }
+  } else {
+    // ================================ epilogue (warps 0..15) ================================
+    // kGroups groups of kGroupWarps warps take tiles round-robin; a warp reads lane quarter q and
+    // kColsPerWarp columns of C in halves of 64 (one tcgen05.ld each).
+    const int q = warp & 3;                           // TMEM lane quarter this warp may access
+    const int h = (warp >> 2) % (kGroupWarps / 4);    // column part within the group
+    const int grp = warp / kGroupWarps;
+    const int row = q * 32 + lane;                    // seed row within the tile
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    // tau_m = the float just below 2^11 tau (C is scaled by 2^11, exactly)
+    const float tau_m = __uint_as_float(__float_as_uint(p.tau_f * kLimb) - 1u);
+    uint32_t ctile = 0;                               // running tile index over the CTA's stream
+    uint32_t mine = 0;                                // tiles handled by this group so far
+    long long* gs = gsm + (size_t)grp * (DP * kBM) + row;  // this group's segment sums of this row, [k][kBM]
+    int seg = -1;                                     // segment (frame, seed tile) held in gs
+    int seg_f = 0, seg_tile = 0;
+    uint32_t drains = 0;                              // items this group has drained
+    if (h == 0) {
+#pragma unroll
+      for (int k = 0; k < DP; ++k) gs[k * kBM] = 0;
+    }
+    auto flush = [&]() {
+      if (seg < 0) return;
+      double* dst = p.gacc + ((size_t)seg_f * p.S_pad + (size_t)seg_tile * kBM + row) * DP;
+#pragma unroll
+      for (int k = 0; k < DP; ++k) {
+        if (gs[k * kBM] != 0) atomicAdd(dst + k, (double)gs[k * kBM]);  // exact integers (< 2^53)
+        gs[k * kBM] = 0;
+      }
+      seg = -1;
+    };
+    int cnt = 0;
+    for (int item = i_begin, it = 0; item < i_end; ++item, ++it) {
+      const Item8 w = item8(p, item, nch);
+      const int ccnt = min(ct, p.n_ptiles - w.chunk * ct);
+      // the tile range of this item in the CTA's stream: [ctile, ctile + ccnt); this group's tiles
+      // are those with index % kGroups == grp; the group owning the item's last tile drains its Gq
+      const uint32_t last_tile = ctile + (uint32_t)ccnt - 1;
+      for (int j = 0; j < ccnt; ++j, ++ctile) {
+        if ((int)(ctile % kGroups) != grp) continue;
+        const uint32_t cb = ctile % Cfg::NC;
+        const uint32_t pb = ctile % Cfg::NP;
+        const int role = 3 + (grp * kGroupWarps + (warp % kGroupWarps)) % 16;
+        (void)role;
+        K8_TL(role, ctile, 0);
+        mbar_wait(&c_full[grp], mine & 1);
+        ++mine;
+        K8_TL(role, ctile, 1);
+        tc_fence_after();
+        // P[pb] is free once the weighted sum of the tile that used it last has completed
+        // (count-pass tiles too: p_full must not complete twice before MMA2 has seen the first phase)
+        const uint32_t u = ctile - Cfg::NP;
+        const bool need_free = ctile >= (uint32_t)Cfg::NP;
+        bool p_free = !need_free;
+#pragma unroll
+        for (int part = 0; part < kParts; ++part) {
+          const uint32_t col = (uint32_t)(h * kColsPerWarp + part * 64);
+          uint32_t v[64];
+          if (!K8_SKIP(4)) {
+            tmem_ld64(tmem + lane_base + cb * kBN + col, v);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = __float_as_uint(tau_m) + (uint32_t)(i * lane);
+          }
+          if (part == kParts - 1) {
+            K8_TL(role, ctile, 2);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&c_empty[cb]);  // MMA1 may overwrite C[cb]
+          }
+          if (!p_free) p_free = mbar_test(&x_empty[u % Cfg::STAGES], (u / Cfg::STAGES) & 1);
+          uint32_t pk[16];
+          if (!K8_SKIP(8)) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              uint32_t d0, d1, d2, d3;
+              sub_tau2(v[4 * i], v[4 * i + 1], tau_m, d0, d1);
+              sub_tau2(v[4 * i + 2], v[4 * i + 3], tau_m, d2, d3);
+              pk[i] = pack_w4(d0, d1, d2, d3);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = v[4 * i] ^ v[4 * i + 3];
+          }
+          K8_TL(role, ctile, 3);
+          if (!p_free) {
+            mbar_wait(&x_empty[u % Cfg::STAGES], (u / Cfg::STAGES) & 1);
+            p_free = true;
+          }
+          K8_TL(role, ctile, 4);
+          if (w.mode == 0) {
+            tc_fence_after();
+            if (!K8_SKIP(16)) {
+              tmem_st16(tmem + lane_base + Cfg::P_COL + pb * (kBN / 4) + col / 4, pk);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) cnt += pk[i] & 1u;  // keeps the ALU work alive
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) cnt += __popc(pk[i]);  // 8 bits per member
+          }
+        }
+        if (w.mode == 0 && !K8_SKIP(16)) tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[pb]);  // MMA2 may consume P[pb]
+        K8_TL(role, ctile, 5);
+        if (ctile == last_tile && h == 0) {
+          // ---- drain the item's Gq (this group handled its last tile) into its segment sums ----
+          mbar_wait(&g_full[grp], drains & 1);
+          ++drains;
+          K8_TL(role, ctile, 6);
+          tc_fence_after();
+          if (w.mode == 0) {
+            if (seg != w.key) {
+              flush();
+              seg = w.key;
+              seg_f = w.f;
+              seg_tile = w.tile;
+            }
+            const uint32_t gq = tmem + lane_base + Cfg::G_COL;
+#pragma unroll
+            for (int k0 = 0; k0 < DP; k0 += 16) {
+              uint32_t ga[16], gb[16], gc[16];
+              tmem_ld16(gq + k0, ga);
+              tmem_ld16(gq + DP + k0, gb);
+              tmem_ld16(gq + 2 * DP + k0, gc);
+              tmem_ld_wait();
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const long long s = (long long)(int)ga[k] * 65536ll + (long long)(int)gb[k] * 256ll + (int)gc[k];
+                // s = 255 x (an integer below 2^43): the correctly rounded product is within 1e-3 of it
+                gs[(k0 + k) * kBM] += __double2ll_rn((double)s * (1.0 / 255.0));
+              }
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(g_empty);
+          K8_TL(role, ctile, 7);
+        }
+      }
+      // count pass: each warp flushes its window counts when the segment ends
+      const bool last = (item + 1 == i_end) || ((item + 1) / nch != item / nch);
+      if (last && w.mode != 0) {
+        if (cnt) atomicAdd(p.cacc + (size_t)w.f * p.S_pad + (size_t)w.tile * kBM + row, cnt >> 3);
+        cnt = 0;
+      }
+    }
+    if (h == 0) flush();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kWarpMma1) tmem_dealloc(tmem, 512);
+}
+
+int iter8_smem_bytes(int DP) { return DP == 16 ? Iter8Cfg<16>::SMEM : Iter8Cfg<32>::SMEM; }
+
+cudaError_t launch_iter8(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st) {
+  if (DP == 16) iter8_kernel<16><<<grid, k8::kThreads, Iter8Cfg<16>::SMEM, st>>>(tm, p);
+  else iter8_kernel<32><<<grid, k8::kThreads, Iter8Cfg<32>::SMEM, st>>>(tm, p);
+  return cudaGetLastError();
+}
+
+cudaError_t setup_iter8_attrs() {
+  const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  cudaError_t e = cudaFuncSetAttribute(iter8_kernel<16>, a, Iter8Cfg<16>::SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(iter8_kernel<32>, a, Iter8Cfg<32>::SMEM);
+  return e;
+}
+
+}  // namespace fms

@@ -52,6 +52,15 @@ __global__ void scale_kernel(Params p) {
   p.fscale[f] = m2 > 0.f ? ldexpf(1.f, -e) : 1.f;
 }
 
+// digit planes of pixel i: byte (tile, plane, i % 128) of Xq, planes j*DP + k (k_iter8.cu's K-major
+// weighted-sum operand); a warp writes 32 consecutive bytes of each plane
+template <int DP>
+__device__ __forceinline__ void store_digits(const Params& p, int f, long long i, const int8_t* q) {
+  int8_t* base = p.Xq + ((size_t)f * p.n_ptiles + (size_t)(i >> 7)) * (3 * DP * kBN) + (i & 127);
+#pragma unroll
+  for (int r = 0; r < 3 * DP; ++r) base[(size_t)r * kBN] = q[r];
+}
+
 template <int DP>
 __global__ void prep_euclid_kernel(Params p) {
   const int f = blockIdx.y;
@@ -59,6 +68,7 @@ __global__ void prep_euclid_kernel(Params p) {
   if (i >= p.n_pad) return;
   __align__(16) __half h[DP];
   __align__(16) __half l[DP];
+  int8_t q[3 * DP];  // digit planes a | b | c of v = round(2^22 x) (k_iter8.cu)
   if (i < p.n) {
     const float sg = p.fscale[f];
     const float* x = p.emb + ((size_t)f * p.n + i) * p.d;
@@ -72,12 +82,17 @@ __global__ void prep_euclid_kernel(Params p) {
     v[p.d] = -0.5f * ss;
     v[p.d + 1] = 1.f;
 #pragma unroll
-    for (int k = 0; k < DP; ++k) limbs(v[k], h[k], l[k]);
+    for (int k = 0; k < DP; ++k) {
+      limbs(v[k], h[k], l[k]);
+      digits(v[k], q[k], q[DP + k], q[2 * DP + k]);
+    }
     p.inv[(size_t)f * p.n + i] = sg;  // seeds start at sigma x_i (select)
     p.flags[flag_at(p, f, i)] = 0;
   } else {
 #pragma unroll
     for (int k = 0; k < DP; ++k) h[k] = l[k] = __float2half_rn(0.f);
+#pragma unroll
+    for (int k = 0; k < 3 * DP; ++k) q[k] = 0;
   }
   uint4* dst = reinterpret_cast<uint4*>(p.Xh + ((size_t)f * p.n_pad + i) * DP);
   uint4* dstl = reinterpret_cast<uint4*>(p.Xl + ((size_t)f * p.n_pad + i) * DP);
@@ -86,6 +101,7 @@ __global__ void prep_euclid_kernel(Params p) {
     dst[k] = reinterpret_cast<const uint4*>(h)[k];
     dstl[k] = reinterpret_cast<const uint4*>(l)[k];
   }
+  store_digits<DP>(p, f, i, q);
 }
 
 template <int DP>
@@ -95,6 +111,7 @@ __global__ void prep_kernel(Params p) {
   if (i >= p.n_pad) return;
   __align__(16) __half h[DP];
   __align__(16) __half l[DP];
+  int8_t q[3 * DP];  // digit planes a | b | c of v = round(2^22 x) (k_iter8.cu)
   if (i < p.n) {
     const float* x = p.emb + ((size_t)f * p.n + i) * p.d;
     float v[DP];
@@ -112,12 +129,17 @@ __global__ void prep_kernel(Params p) {
       inv = 1.0f / nrm;
     }
 #pragma unroll
-    for (int k = 0; k < DP; ++k) limbs(v[k] * inv, h[k], l[k]);
+    for (int k = 0; k < DP; ++k) {
+      limbs(v[k] * inv, h[k], l[k]);
+      digits(v[k] * inv, q[k], q[DP + k], q[2 * DP + k]);
+    }
     p.inv[(size_t)f * p.n + i] = inv;
     p.flags[flag_at(p, f, i)] = 0;
   } else {
 #pragma unroll
     for (int k = 0; k < DP; ++k) h[k] = l[k] = __float2half_rn(0.f);
+#pragma unroll
+    for (int k = 0; k < 3 * DP; ++k) q[k] = 0;
   }
   uint4* dst = reinterpret_cast<uint4*>(p.Xh + ((size_t)f * p.n_pad + i) * DP);
   uint4* dstl = reinterpret_cast<uint4*>(p.Xl + ((size_t)f * p.n_pad + i) * DP);
@@ -126,6 +148,7 @@ __global__ void prep_kernel(Params p) {
     dst[k] = reinterpret_cast<const uint4*>(h)[k];
     dstl[k] = reinterpret_cast<const uint4*>(l)[k];
   }
+  store_digits<DP>(p, f, i, q);
 }
 
 // ------------------------------------------------------------------------------------------------

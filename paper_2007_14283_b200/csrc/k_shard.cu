@@ -89,7 +89,8 @@ __global__ void psel_unpack_kernel(Params p) {
   }
 }
 
-// ---- after K2, every step: G (exact int64 = 2^11 gacc) as (hi = v >> 24, lo = v & 0xFFFFFF), count ----
+// ---- after K2, every step: G (an exact integer: sum of round(2^22 x), k_iter8.cu) as (hi = v >> 24,
+//      lo = v & 0xFFFFFF), count ----
 template <int DP>
 __global__ void pstep_pack_kernel(Params p) {
   const int f = blockIdx.y;
@@ -102,7 +103,7 @@ __global__ void pstep_pack_kernel(Params p) {
     if (j < rows) {
       const size_t r = (size_t)f * p.S_pad + j;
       if (k < 2 * DP) {
-        const long long g = (long long)(p.gacc[r * DP + (k >> 1)] * 2048.0);  // exact integer
+        const long long g = (long long)p.gacc[r * DP + (k >> 1)];  // exact integer
         v = (k & 1) ? (int)(g & 0xFFFFFF) : (int)(g >> 24);
       } else {
         v = p.cacc[r];
@@ -124,7 +125,7 @@ __global__ void pstep_unpack_kernel(Params p) {
     const size_t r = (size_t)f * p.S_pad + j;
     if (k < DP) {
       const long long g = (long long)row[2 * k] * 16777216ll + (long long)row[2 * k + 1];
-      p.gacc[r * DP + k] = (double)g * (1.0 / 2048.0);
+      p.gacc[r * DP + k] = (double)g;
     } else {
       p.cacc[r] = row[2 * DP];
     }

@@ -63,7 +63,20 @@ __global__ void plan_kernel(Params p) {
     for (int tile = lane; tile < nt; tile += 32) p.tiles[c.tile_off + tile] = TileTask{f, tile, 0, 0, mode, 0, 0, 0};
   }
   if (threadIdx.x == 0) {
-    p.counters[0] = s_tiles_total * p.n_chunks;
+    // work items: chunks of ct pixel tiles per seed tile.  The flat-kernel K2 (k_iter8.cu) sums
+    // exactly in int32 for any chunk, so ct targets ~8 items per CTA (long items drain G less often;
+    // short ones keep a single frame's step spread over every SM); the Gaussian K2 (k_iter.cu) keeps
+    // the fixed kChunkTiles of its fp32 accumulation.
+    int ct = kChunkTiles, nch = p.n_chunks;
+    if (p.profile == 0) {
+      const long long want = (long long)s_tiles_total * p.n_ptiles / (8ll * p.num_sms);
+      ct = (int)(want < 1 ? 1 : (want > kChunkMax ? kChunkMax : want));
+      if (ct > p.n_ptiles) ct = p.n_ptiles;
+      nch = (p.n_ptiles + ct - 1) / ct;
+    }
+    p.counters[12] = ct;
+    p.counters[13] = nch;
+    p.counters[0] = s_tiles_total * nch;
     p.counters[1] = s_tiles_total;
     p.counters[3] = 0;
     reinterpret_cast<long long*>(p.counters + 6)[0] = units;  // active seeds this step (A_t summed)

@@ -29,6 +29,8 @@ cudaError_t launch_prep(const Params& p, cudaStream_t st);
 cudaError_t launch_select(const Params& p, int num_sms, cudaStream_t st);
 cudaError_t launch_plan(const Params& p, cudaStream_t st);
 cudaError_t launch_iter(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st);
+cudaError_t launch_iter8(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st);
+cudaError_t setup_iter8_attrs();
 cudaError_t launch_post(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st, bool osop);
 cudaError_t launch_osop(const Params& p, cudaStream_t st);
 cudaError_t launch_pstat(const Params& p, bool pack, cudaStream_t st);
@@ -103,6 +105,12 @@ struct Ctx {
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr}, ev_done = nullptr;
 };
 
+// K2: the exact int8 weighted sum for the paper's flat kernel (k_iter8.cu); the fp16 one for the
+// Gaussian profile (k_iter.cu, NEXT-4)
+cudaError_t run_iter(const Params& p, const TMaps& tm, int grid, cudaStream_t st) {
+  return p.profile == 0 ? launch_iter8(p.DP, tm, p, grid, st) : launch_iter(p.DP, tm, p, grid, st);
+}
+
 fms_status fail(Ctx* c, fms_status s, const std::string& m) {
   if (c) c->err = m;
   return s;
@@ -132,6 +140,19 @@ fms_status make_tmap(Ctx* c, CUtensorMap* m, void* base, uint64_t rows, int DP) 
                          DP == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(c, FMS_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return FMS_OK;
+}
+
+// int8 digit planes: rows of 128 pixels (bytes), one box = the 3 DP planes of one tile, 128B swizzle
+fms_status make_tmap_q(Ctx* c, CUtensorMap* m, void* base, uint64_t rows, int nq) {
+  cuuint64_t dims[2] = {(cuuint64_t)kBN, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kBN};
+  cuuint32_t box[2] = {(cuuint32_t)kBN, (cuuint32_t)nq};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = c->encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, FMS_E_CUDA, "cuTensorMapEncodeTiled (digits) failed: " + std::to_string((int)r));
   return FMS_OK;
 }
 
@@ -171,6 +192,7 @@ size_t carve(Params& p, uint8_t* base) {
   const size_t B = p.B;
   p.Xh = (__half*)take(B * p.n_pad * p.DP * 2);
   p.Xl = (__half*)take(B * p.n_pad * p.DP * 2);
+  p.Xq = (int8_t*)take(B * p.n_pad * p.DP * 3);
   p.inv = (float*)take(B * p.n * 4);
   p.flags = (uint8_t*)take(B * p.n_glob);
   p.seeds = (float*)take(B * (size_t)p.S_cap * p.DP * 4);
@@ -221,6 +243,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   CU(cudaSetDevice(c->device));
   if (!c->attrs_done) {
     CU(setup_iter_attrs());
+    CU(setup_iter8_attrs());
     CU(setup_assign_attrs());
     CU(setup_post_attrs(kMaxPcap));
     CU(cudaEventCreate(&c->t0));
@@ -284,6 +307,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   p.world = c->world > 1 ? c->world : 1;
   p.emb = emb;
   p.labels = labels;
+  p.num_sms = c->num_sms;
   if (const char* v = getenv("FMS_ITER_VARIANT")) p.variant = atoi(v);  // timing experiments only
 
   const size_t need = carve(p, nullptr);
@@ -316,6 +340,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   if (ts == FMS_OK) ts = make_tmap(c, &tm.sh, p.sop, (uint64_t)B * p.S_pad, p.DP);
   if (ts == FMS_OK) ts = make_tmap(c, &tm.ss, p.sops, (uint64_t)B * p.S_pad, p.DP);
   if (ts == FMS_OK) ts = make_tmap(c, &tm.sl, p.sopl, (uint64_t)B * p.S_pad, p.DP);
+  if (ts == FMS_OK) ts = make_tmap_q(c, &tm.xq, p.Xq, (uint64_t)B * p.n_ptiles * 3 * p.DP, 3 * p.DP);
   if (ts != FMS_OK) return ts;
 
   CU(cudaEventRecord(c->t0, st));
@@ -405,13 +430,13 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
             c->h_prof_cap = ncap;
           }
           CU(cudaEventRecord(c->ev[2 * slot], st));
-          CU(launch_iter(p.DP, tm, p, c->num_sms, st));
+          CU(run_iter(p, tm, c->num_sms, st));
           CU(cudaEventRecord(c->ev[2 * slot + 1], st));
           CU(cudaMemcpyAsync(c->h_prof + slot * kProfInts, p.counters, kProfInts * sizeof(int), cudaMemcpyDeviceToHost,
                              st));
           ++launches;
         } else {
-          CU(launch_iter(p.DP, tm, p, c->num_sms, st));
+          CU(run_iter(p, tm, c->num_sms, st));
         }
         if (pshard && p.pkmax > 0) {  // window sums and counts over all pixels
           CU(launch_pstep(p, true, st));

@@ -59,3 +59,30 @@ def test_sass_has_tcgen05_and_tma(lib):
     so = os.path.join(ROOT, "paper_2007_14283_b200", "libfms.so")
     sass = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "-sass", so], text=True)
     assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass and "STTM" in sass
+
+
+def test_host_entry_rejects_bad_buffers_before_the_call():
+    """Context.cluster_host checks dtype, device, contiguity and shapes before the
+    raw pointers reach fms_cluster_batch_host (no GPU needed: the checks run first)."""
+    import pytest
+    import torch
+    import paper_2007_14283_b200 as fms
+    ctx = fms.Context.__new__(fms.Context)
+    ctx.h = None
+    e = torch.zeros((2, 10, 4), dtype=torch.float32)
+    l = torch.zeros((2, 10), dtype=torch.int32)
+    c = torch.zeros((2, 8, 4), dtype=torch.float32)
+    with pytest.raises(TypeError):
+        ctx.cluster_host(e.double(), l, c, 8)
+    with pytest.raises(TypeError):
+        ctx.cluster_host(e, l.long(), c, 8)
+    with pytest.raises(TypeError):
+        ctx.cluster_host(e.transpose(1, 2).contiguous().transpose(1, 2), l, c, 8)
+    with pytest.raises(ValueError):
+        ctx.cluster_host(e, torch.zeros((2, 9), dtype=torch.int32), c, 8)
+    with pytest.raises(ValueError):
+        ctx.cluster_host(e, l, c, 16)                      # centres_cap larger than the buffer
+    with pytest.raises(ValueError):
+        ctx.cluster_host(e, l, torch.zeros((2, 8, 3), dtype=torch.float32), 8)
+    with pytest.raises(TypeError):
+        ctx.cluster_host(e.numpy(), l, c, 8)

@@ -111,3 +111,61 @@ def test_pixel_sharded_matches_oracle_exact():
     assert bijection(labels, ro.labels)
     _, _, dist = match_centres(parts[1]["centres"][0, :ro.K], ro.centres)
     assert dist.max() <= 1e-4
+
+
+def _host_worker(rank, world, port, out):
+    """Host-buffer entry on a pixel-sharded context: a plain host call first (creates the copy stream),
+    then pixel sharding (grows the exchange buffer) and two sharded host calls, then the device entry;
+    finally the context is destroyed.  Results of all sharded calls must agree."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2007_14283_b200 as fms
+    from paper_2007_14283_b200.dist import enable_pixel_sharding
+    X = _inputs("S1", [3, 4])
+    B, n, d = X.shape
+    pol = fms.default_policy(**_policy_kw("S1", n))
+    ctx = fms.Context(0)
+    eh = torch.from_numpy(X).pin_memory()
+    lh = torch.empty((B, n), dtype=torch.int32).pin_memory()
+    ch = torch.zeros((B, 256, d), dtype=torch.float32).pin_memory()
+    ctx.cluster_host(eh, lh, ch, 256, policy=pol)   # unsharded host call: copy stream + events exist
+    lo, hi = enable_pixel_sharding(ctx, n)
+    ehs = torch.from_numpy(np.ascontiguousarray(X[:, lo:hi])).pin_memory()
+    res = []
+    for _ in range(2):
+        lhs = torch.full((B, hi - lo), -1, dtype=torch.int32).pin_memory()
+        chs = torch.zeros((B, 256, d), dtype=torch.float32).pin_memory()
+        _, K, _ = ctx.cluster_host(ehs, lhs, chs, 256, policy=pol)
+        res.append((lhs.clone(), chs.clone(), K))
+    ld, cd, Kd, _ = ctx.cluster(torch.from_numpy(np.ascontiguousarray(X[:, lo:hi])).cuda(), policy=pol, centres_cap=256)
+    ctx.close()
+    np.savez(os.path.join(out, f"h{rank}.npz"), l0=res[0][0].numpy(), l1=res[1][0].numpy(), ld=ld.cpu().numpy(),
+             c0=res[0][1].numpy(), c1=res[1][1].numpy(), cd=cd.cpu().numpy(), K0=np.array(res[0][2]),
+             K1=np.array(res[1][2]), Kd=np.array(Kd), lo=lo, hi=hi)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_pixel_sharded_host_entry_and_teardown():
+    """VERDICT r01 weak #7 / ADVICE high: the pixel-shard buffer growth used to destroy the host entry's
+    copy stream and events; a pixel-sharded host call then used dead handles."""
+    import torch
+    import torch.multiprocessing as mp
+    import paper_2007_14283_b200 as fms
+    X = _inputs("S1", [3, 4])
+    pol = fms.default_policy(**_policy_kw("S1", X.shape[1]))
+    rl, rc, rK, _ = fms.cluster(torch.from_numpy(X).cuda(), policy=pol, centres_cap=256)
+    ref = dict(labels=rl.cpu().numpy(), centres=rc.cpu().numpy(), K=np.array(rK))
+    with tempfile.TemporaryDirectory() as out:
+        mp.start_processes(_host_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
+        parts = [dict(np.load(os.path.join(out, f"h{r}.npz"))) for r in range(2)]
+    for key in ("l0", "l1", "ld"):
+        assert np.array_equal(np.concatenate([r[key] for r in parts], axis=1), ref["labels"]), key
+    for r in parts:
+        for key in ("K0", "K1", "Kd"):
+            assert np.array_equal(r[key], ref["K"]), key
+        for key in ("c0", "c1", "cd"):
+            assert np.array_equal(r[key][:, :256], ref["centres"][:, :256]), key
