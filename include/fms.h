@@ -87,6 +87,8 @@ typedef struct {
   int64_t iter_items;         /* sum over K2 launches of work items */
   int64_t launches;           /* kernels this library launched during the call */
   int64_t iter_count_units;   /* sum over K2 launches of converged modes counted (intensity pass, R10) */
+  int64_t host_syncs;         /* host waits on the stream during the call: 1 with the device-resident loop
+                                 (option "graph", the default); one per poll with the host-polled loop */
 } fms_run_stats;
 
 fms_status fms_default_policy(fms_seed_policy* out);
@@ -149,7 +151,11 @@ fms_status fms_set_exchange(void* ctx, fms_exchange_fn fn, void* user, int32_t r
 fms_status fms_set_pixel_shard(void* ctx, fms_exchange_fn fn, void* user, int32_t rank, int32_t world,
                                int64_t n_global, int64_t offset);
 
-/* Options: "profile_iter" (0/1): time every K2 launch with CUDA events for fms_run_stats.iter_ms.
+/* Options: "graph" (0/1, default 1): run a single-GPU call as one CUDA graph launch whose round and
+ *          lockstep-step loops are WHILE conditional nodes with device-set conditions (one host
+ *          synchronisation per call); sharded and profiled calls always use the host-polled loop.
+ *          "profile_iter" (0/1): time every K2 launch with CUDA events for fms_run_stats.iter_ms
+ *          (forces the host-polled loop).
  *          "poll_steps" (1..64, default 4): lockstep steps launched between two host polls of the
  *          device counters (a frame that finishes early idles at most poll_steps - 1 steps).
  *          "kernel_profile" (0/1, default 0): the kernel of the mean-shift update.  0 = the paper's

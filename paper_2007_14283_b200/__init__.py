@@ -55,7 +55,8 @@ class FrameStats(C.Structure):
 class RunStats(C.Structure):
     _fields_ = [("ms_total", C.c_double), ("workspace_bytes", C.c_int64), ("steps", C.c_int32),
                 ("iter_launches", C.c_int32), ("iter_ms", C.c_double), ("iter_seed_iters", C.c_int64),
-                ("iter_items", C.c_int64), ("launches", C.c_int64), ("iter_count_units", C.c_int64)]
+                ("iter_items", C.c_int64), ("launches", C.c_int64), ("iter_count_units", C.c_int64),
+                ("host_syncs", C.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(kAsgThreads, 1) assign_tc_kernel(const __grid_
           const size_t pi = (size_t)f * p.n + px;
           const bool covered = best >= tau2;
           p.flags[flag_at(p, f, px)] = (uint8_t)((fl & ~PF_COVERED) | (covered ? PF_COVERED : 0));
-          p.labels[pi] = lab;
+          labels_of(p)[pi] = lab;
           // warp-aggregated histogram: neighbouring pixels mostly share a label, and 32 same-address
           // shared atomics would serialise
           const unsigned same = __match_any_sync(__activemask(), lab);

@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(256) assign_kernel(Params p) {
   const bool euclid = p.metric == 1;
   const float sg = euclid ? p.fscale[f] : 1.f;
   if (valid) {
-    const float* src = p.emb + ((size_t)f * p.n + i) * p.d;
+    const float* src = emb_of(p) + ((size_t)f * p.n + i) * p.d;
 #pragma unroll
     for (int k = 0; k < DP; ++k)
       if (k < p.d) x[k] = src[k] * sg;
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256) assign_kernel(Params p) {
     const bool covered = euclid ? best >= 0.5f * (dotv<DP>(x, x) - (float)(hs * hs)) : best * p.inv[pi] >= p.tau_f;
     const uint8_t fl = p.flags[flag_at(p, f, i)];
     p.flags[flag_at(p, f, i)] = (uint8_t)((fl & ~PF_COVERED) | (covered ? PF_COVERED : 0));
-    p.labels[pi] = lab;
+    labels_of(p)[pi] = lab;
     cand = (!covered && !(fl & PF_VISITED)) ? 1 : 0;
   }
   for (int k0 = 0; k0 < Kc; k0 += kAsgChunk) {
@@ -352,6 +352,7 @@ __global__ void osop_kernel(Params p) {
 
 template <int DP>
 __global__ void output_kernel(Params p, float* centres_out, int cap) {
+  if (!centres_out) centres_out = p.io->centres;  // graph mode
   const int f = blockIdx.y;
   const FrameCtl& c = p.ctl[f];
   const int Kc = c.Kc < cap ? c.Kc : cap;

@@ -33,7 +33,7 @@ __global__ void maxnorm_kernel(Params p) {
   const int f = blockIdx.y;
   float m = 0.f;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += (long long)gridDim.x * blockDim.x) {
-    const float* x = p.emb + ((size_t)f * p.n + i) * p.d;
+    const float* x = emb_of(p) + ((size_t)f * p.n + i) * p.d;
     float ss = 0.f;
     for (int k = 0; k < p.d; ++k) ss = fmaf(x[k], x[k], ss);
     m = fmaxf(m, isfinite(ss) ? ss : INFINITY);
@@ -71,7 +71,7 @@ __global__ void prep_euclid_kernel(Params p) {
   int8_t q[3 * DP];  // digit planes a | b | c of v = round(2^22 x) (k_iter8.cu)
   if (i < p.n) {
     const float sg = p.fscale[f];
-    const float* x = p.emb + ((size_t)f * p.n + i) * p.d;
+    const float* x = emb_of(p) + ((size_t)f * p.n + i) * p.d;
     float v[DP];
     float ss = 0.f;
 #pragma unroll
@@ -113,7 +113,7 @@ __global__ void prep_kernel(Params p) {
   __align__(16) __half l[DP];
   int8_t q[3 * DP];  // digit planes a | b | c of v = round(2^22 x) (k_iter8.cu)
   if (i < p.n) {
-    const float* x = p.emb + ((size_t)f * p.n + i) * p.d;
+    const float* x = emb_of(p) + ((size_t)f * p.n + i) * p.d;
     float v[DP];
     float ss = 0.f;
 #pragma unroll
@@ -341,7 +341,7 @@ __global__ void sel_write_kernel(Params p) {
     const long long il = i - p.pix_off;
     const bool have = il >= 0 && il < p.n;
     const float inv = have ? p.inv[(size_t)f * p.n + il] : 0.f;
-    const float* x = p.emb + ((size_t)f * p.n + (have ? il : 0)) * p.d;
+    const float* x = emb_of(p) + ((size_t)f * p.n + (have ? il : 0)) * p.d;
     float* s = p.seeds + so * DP;
     // the operand row (and accumulators) of an active seed sit at its compacted position; with seed
     // sharding only this rank's seeds (j % world == rank) are active here, at j / world

@@ -31,6 +31,9 @@ cudaError_t launch_plan(const Params& p, cudaStream_t st);
 cudaError_t launch_iter(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st);
 cudaError_t launch_iter8(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st);
 cudaError_t setup_iter8_attrs();
+cudaError_t launch_set_cond(cudaGraphConditionalHandle h, unsigned v, cudaStream_t st);
+cudaError_t launch_step_cond(cudaGraphConditionalHandle h, const Params& p, cudaStream_t st);
+cudaError_t launch_round_cond(cudaGraphConditionalHandle h, const Params& p, cudaStream_t st);
 cudaError_t launch_post(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st, bool osop);
 cudaError_t launch_osop(const Params& p, cudaStream_t st);
 cudaError_t launch_pstat(const Params& p, bool pack, cudaStream_t st);
@@ -103,6 +106,20 @@ struct Ctx {
   int host_chunk = 48;
   cudaStream_t cstream = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr}, ev_done = nullptr;
+  // device-resident loop (k_graph.cu): one CUDA graph per call configuration, cached
+  int use_graph = 1;             // option "graph"
+  cudaStream_t gst[3] = {nullptr, nullptr, nullptr};  // capture streams (prologue, round body, step body)
+  struct GraphEntry {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    Params key{};                // Params the graph was captured with (io buffers zeroed)
+    int cap = -1;
+    unsigned long long used = 0;
+  };
+  static constexpr int kGraphCache = 4;  // the host entry alternates chunk sizes: keep a few graphs
+  GraphEntry gcache[kGraphCache];
+  unsigned long long gclock = 0;
+  IoPtrs* h_io = nullptr;        // pinned: this call's buffers, copied to Params::io before the launch
 };
 
 // K2: the exact int8 weighted sum for the paper's flat kernel (k_iter8.cu); the fp16 one for the
@@ -218,6 +235,7 @@ size_t carve(Params& p, uint8_t* base) {
   p.blkcnt = (int*)take(B * (size_t)p.nblk_glob * 4);
   p.ctl = (FrameCtl*)take(B * sizeof(FrameCtl));
   p.fscale = (float*)take(B * 4);
+  p.io = (const IoPtrs*)take(sizeof(IoPtrs));
   if (p.P_cap > kMaxPcap) {  // merge pool sorted in global memory (Alg. 1)
     p.mkeys = (unsigned long long*)take(B * (size_t)p.P_cap * 8);
     p.mkeys_sorted = (unsigned long long*)take(B * (size_t)p.P_cap * 8);
@@ -232,6 +250,90 @@ size_t carve(Params& p, uint8_t* base) {
     p.xbuf = (int*)take((size_t)B * p.S_cap * (p.DP + 2) * 4);
   }
   return align_up(off, 1024);
+}
+
+// Capture the whole call (prologue, the round loop with the step loop nested in it, output) into a
+// CUDA graph with two WHILE conditional nodes whose conditions the device sets (k_graph.cu).  Body
+// graphs are populated by stream capture on helper streams.
+fms_status build_graph(Ctx* c, const Params& p, const TMaps& tm, int32_t cap, Ctx::GraphEntry& ge) {
+  for (int i = 0; i < 3; ++i)
+    if (!c->gst[i]) CU(cudaStreamCreateWithFlags(&c->gst[i], cudaStreamNonBlocking));
+  if (ge.exec) { cudaGraphExecDestroy(ge.exec); ge.exec = nullptr; }
+  if (ge.graph) { cudaGraphDestroy(ge.graph); ge.graph = nullptr; }
+  ge.cap = -1;
+  cudaStream_t s0 = c->gst[0], s1 = c->gst[1], s2 = c->gst[2];
+  const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
+  // at the current capture position of `s`: a kernel setting the new condition to 1, then a WHILE
+  // node on it; returns the node's body graph
+  auto add_while = [&](cudaStream_t s, cudaGraphConditionalHandle* h, cudaGraph_t* body) -> fms_status {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    CU(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &ndeps));
+    CU(cudaGraphConditionalHandleCreate(h, g, 0, 0));
+    CU(launch_set_cond(*h, 1u, s));
+    CU(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &ndeps));
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = *h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CU(cudaGraphAddNode(&node, g, deps, ndeps, &np));
+    *body = np.conditional.phGraph_out[0];
+    CU(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+    return FMS_OK;
+  };
+  cudaGraphConditionalHandle h_round, h_step;
+  cudaGraph_t round_body = nullptr, step_body = nullptr;
+  CU(cudaStreamBeginCapture(s0, mode));
+  fms_status r = [&]() -> fms_status {
+    CU(cudaMemsetAsync(p.counters, 0, kCounters * 4, s0));
+    CU(launch_prep(p, s0));
+    fms_status q = add_while(s0, &h_round, &round_body);
+    if (q != FMS_OK) return q;
+    // ---- round body: select, the step loop, merge / assign / OSOP ----
+    CU(cudaStreamBeginCaptureToGraph(s1, round_body, nullptr, nullptr, 0, mode));
+    q = [&]() -> fms_status {
+      CU(launch_select(p, c->num_sms, s1));
+      fms_status q2 = add_while(s1, &h_step, &step_body);
+      if (q2 != FMS_OK) return q2;
+      // ---- step body ----
+      CU(cudaStreamBeginCaptureToGraph(s2, step_body, nullptr, nullptr, 0, mode));
+      q2 = [&]() -> fms_status {
+        CU(launch_plan(p, s2));
+        CU(run_iter(p, tm, c->num_sms, s2));
+        CU(launch_update(p, c->num_sms, s2));
+        CU(launch_ctl(p, s2));
+        CU(launch_step_cond(h_step, p, s2));
+        return FMS_OK;
+      }();
+      cudaGraph_t gdone = nullptr;
+      const cudaError_t e2 = cudaStreamEndCapture(s2, &gdone);
+      if (q2 != FMS_OK) return q2;
+      CU(e2);
+      CU(launch_post(p, tm, c->num_sms, s1, true));
+      CU(launch_round_cond(h_round, p, s1));
+      return FMS_OK;
+    }();
+    cudaGraph_t gdone = nullptr;
+    const cudaError_t e1 = cudaStreamEndCapture(s1, &gdone);
+    if (q != FMS_OK) return q;
+    CU(e1);
+    if (cap > 0) CU(launch_output(p, nullptr, cap, s0));
+    return FMS_OK;
+  }();
+  const cudaError_t e0 = cudaStreamEndCapture(s0, &ge.graph);
+  if (r != FMS_OK) {
+    cudaGetLastError();
+    return r;
+  }
+  CU(e0);
+  CU(cudaGraphInstantiate(&ge.exec, ge.graph, 0));
+  ge.key = p;
+  ge.cap = cap;
+  return FMS_OK;
 }
 
 fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, double h, int32_t max_iters,
@@ -308,7 +410,6 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   p.emb = emb;
   p.labels = labels;
   p.num_sms = c->num_sms;
-  if (const char* v = getenv("FMS_ITER_VARIANT")) p.variant = atoi(v);  // timing experiments only
 
   const size_t need = carve(p, nullptr);
   if (need > c->ws_bytes) {
@@ -350,151 +451,193 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
     CU(cudaMemsetAsync(p.cacc, 0, (size_t)B * p.S_pad * 4, st));
     c->fresh_ws = false;
   }
-  auto pgrow = [&](size_t ints) -> fms_status {  // pixel-sharding exchange buffer
-    const size_t bytes = std::max<size_t>(ints, 1) * 4;
-    if (bytes > c->pbuf_bytes) {
-      CU(cudaStreamSynchronize(st));
-      if (c->pbuf) cudaFree(c->pbuf);
-      c->pbuf = nullptr;
-      c->pbuf_bytes = 0;
-      if (cudaMalloc(&c->pbuf, bytes) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(c, FMS_E_OOM, "pixel-shard exchange buffer allocation failed");
-      }
-      c->pbuf_bytes = bytes;
-    }
-    p.pbuf = reinterpret_cast<int*>(c->pbuf);
-    return FMS_OK;
-  };
-  auto pxchg = [&](size_t ints, const char* what) -> fms_status {
-    if (c->pfn(c->puser, p.pbuf, (int64_t)ints, st) != 0) return fail(c, FMS_E_NCCL, std::string(what) + " exchange failed");
-    return FMS_OK;
-  };
-  const size_t post_ints = (size_t)B * ((size_t)p.C_cap + 2 + p.pcov_words);
-  if (pshard) {
-    CU(cudaMemsetAsync(p.flags, 0, (size_t)B * p.n_glob, st));  // other ranks' pixels: filled by exchanges
-    fms_status g = pgrow(std::max<size_t>(post_ints, B));
-    if (g != FMS_OK) return g;
-  }
-  CU(launch_prep(p, st));
-  if (pshard) {  // a zero-norm row on any rank fails the frame on every rank
-    CU(launch_pstat(p, true, st));
-    fms_status g = pxchg(B, "status");
-    if (g != FMS_OK) return g;
-    CU(launch_pstat(p, false, st));
-  }
+  // one call on one GPU without per-launch profiling runs as one CUDA graph launch with the round
+  // and step loops on the device (k_graph.cu); sharded calls (a collective between kernels) and
+  // profiled calls run the host-polled loop below
+  const bool gmode = c->use_graph && !pshard && p.world == 1 && !c->profile;
   int steps = 0, launches = 0;
   long long kernels = 2;  // init + prep
-  std::vector<int> prof_slots;
-  for (int round = 0; round < pol->max_rounds + 1; ++round) {
-    CU(launch_select(p, c->num_sms, st));
-    kernels += 7;
-    if (pshard) {  // the round's seed rows come from the ranks holding the seed pixels
-      CU(launch_psel_kmax(p, st));
-      CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
-      CU(cudaStreamSynchronize(st));
-      p.pkmax = c->h_counters[8];
-      fms_status g = pgrow(std::max(post_ints, (size_t)B * p.pkmax * (2 * p.DP + 1)));
+  long long syncs = 0;    // host waits on the stream during the call
+  if (gmode) {
+    Params key = p;
+    key.emb = nullptr;
+    key.labels = nullptr;
+    Ctx::GraphEntry* ge = nullptr;
+    for (auto& e : c->gcache)
+      if (e.exec && e.cap == cap && memcmp(&key, &e.key, sizeof(Params)) == 0) ge = &e;
+    if (!ge) {  // capture a new graph into the least recently used slot
+      ge = &c->gcache[0];
+      for (auto& e : c->gcache)
+        if (e.used < ge->used) ge = &e;
+      fms_status g = build_graph(c, key, tm, cap, *ge);
       if (g != FMS_OK) return g;
-      if (p.pkmax > 0) {
-        CU(launch_psel(p, true, st));
-        g = pxchg((size_t)B * p.pkmax * p.DP, "seed");
-        if (g != FMS_OK) return g;
-        CU(launch_psel(p, false, st));
-        kernels += 2;
-      }
-      kernels += 1;
     }
-    for (int s = 0; s < max_iters + c->poll; s += c->poll) {
-      for (int k = 0; k < c->poll; ++k) {
-        CU(launch_plan(p, st));
-        if (c->profile) {
-          const size_t slot = launches;
-          if (c->ev.size() < 2 * (slot + 1)) {
-            cudaEvent_t e0, e1;
-            CU(cudaEventCreate(&e0));
-            CU(cudaEventCreate(&e1));
-            c->ev.push_back(e0);
-            c->ev.push_back(e1);
-          }
-          if (c->h_prof_cap < slot + 1) {
-            size_t ncap = std::max<size_t>(256, 2 * (slot + 1));
-            int* np = nullptr;
-            CU(cudaMallocHost(&np, ncap * kProfInts * sizeof(int)));
-            if (c->h_prof) {
-              CU(cudaStreamSynchronize(st));
-              memcpy(np, c->h_prof, c->h_prof_cap * kProfInts * sizeof(int));
-              cudaFreeHost(c->h_prof);
-            }
-            c->h_prof = np;
-            c->h_prof_cap = ncap;
-          }
-          CU(cudaEventRecord(c->ev[2 * slot], st));
-          CU(run_iter(p, tm, c->num_sms, st));
-          CU(cudaEventRecord(c->ev[2 * slot + 1], st));
-          CU(cudaMemcpyAsync(c->h_prof + slot * kProfInts, p.counters, kProfInts * sizeof(int), cudaMemcpyDeviceToHost,
-                             st));
-          ++launches;
-        } else {
-          CU(run_iter(p, tm, c->num_sms, st));
+    ge->used = ++c->gclock;
+    if (!c->h_io) CU(cudaMallocHost(&c->h_io, sizeof(IoPtrs)));
+    *c->h_io = IoPtrs{emb, labels, centres};
+    CU(cudaMemcpyAsync((void*)p.io, c->h_io, sizeof(IoPtrs), cudaMemcpyHostToDevice, st));
+    CU(cudaGraphLaunch(ge->exec, st));
+  } else {
+    p.io = nullptr;
+    auto pgrow = [&](size_t ints) -> fms_status {  // pixel-sharding exchange buffer
+      const size_t bytes = std::max<size_t>(ints, 1) * 4;
+      if (bytes > c->pbuf_bytes) {
+        CU(cudaStreamSynchronize(st));
+        ++syncs;
+        if (c->pbuf) cudaFree(c->pbuf);
+        c->pbuf = nullptr;
+        c->pbuf_bytes = 0;
+        if (cudaMalloc(&c->pbuf, bytes) != cudaSuccess) {
+          cudaGetLastError();
+          return fail(c, FMS_E_OOM, "pixel-shard exchange buffer allocation failed");
         }
-        if (pshard && p.pkmax > 0) {  // window sums and counts over all pixels
-          CU(launch_pstep(p, true, st));
-          fms_status g = pxchg((size_t)B * p.pkmax * (2 * p.DP + 1), "step");
+        c->pbuf_bytes = bytes;
+      }
+      p.pbuf = reinterpret_cast<int*>(c->pbuf);
+      return FMS_OK;
+    };
+    auto pxchg = [&](size_t ints, const char* what) -> fms_status {
+      if (c->pfn(c->puser, p.pbuf, (int64_t)ints, st) != 0) return fail(c, FMS_E_NCCL, std::string(what) + " exchange failed");
+      return FMS_OK;
+    };
+    const size_t post_ints = (size_t)B * ((size_t)p.C_cap + 2 + p.pcov_words);
+    if (pshard) {
+      CU(cudaMemsetAsync(p.flags, 0, (size_t)B * p.n_glob, st));  // other ranks' pixels: filled by exchanges
+      fms_status g = pgrow(std::max<size_t>(post_ints, B));
+      if (g != FMS_OK) return g;
+    }
+    CU(launch_prep(p, st));
+    if (pshard) {  // a zero-norm row on any rank fails the frame on every rank
+      CU(launch_pstat(p, true, st));
+      fms_status g = pxchg(B, "status");
+      if (g != FMS_OK) return g;
+      CU(launch_pstat(p, false, st));
+    }
+    for (int round = 0; round < pol->max_rounds + 1; ++round) {
+      CU(launch_select(p, c->num_sms, st));
+      kernels += 7;
+      if (pshard) {  // the round's seed rows come from the ranks holding the seed pixels
+        CU(launch_psel_kmax(p, st));
+        CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        ++syncs;
+        p.pkmax = c->h_counters[8];
+        fms_status g = pgrow(std::max(post_ints, (size_t)B * p.pkmax * (2 * p.DP + 1)));
+        if (g != FMS_OK) return g;
+        if (p.pkmax > 0) {
+          CU(launch_psel(p, true, st));
+          g = pxchg((size_t)B * p.pkmax * p.DP, "seed");
           if (g != FMS_OK) return g;
-          CU(launch_pstep(p, false, st));
+          CU(launch_psel(p, false, st));
           kernels += 2;
         }
-        CU(launch_update(p, c->num_sms, st));
-        if (p.world > 1) {  // seed sharding: per-frame step counts summed over the ranks
-          CU(launch_xchg_pack(p, st));
-          if (c->xfn(c->xuser, p.xchg, (int64_t)B * 4, st) != 0) return fail(c, FMS_E_NCCL, "step exchange failed");
-        }
-        CU(launch_ctl(p, st));
-        ++steps;
-        kernels += p.world > 1 ? 5 : 4;  // plan, iter, update, (exchange pack), ctl_step
+        kernels += 1;
       }
-      CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
-      CU(cudaStreamSynchronize(st));
-      if (c->h_counters[5]) return fail(c, FMS_E_INTERNAL, "work-item capacity exceeded");
-      if (c->h_counters[3] == 0) break;  // no frame still iterating
-    }
-    if (p.world > 1) {  // seed sharding: every rank gets every owner's converged seeds before the merge
-      CU(launch_xkmax(p, st));
-      CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
-      CU(cudaStreamSynchronize(st));
-      p.xkmax = c->h_counters[8];
-      if (p.xkmax > 0) {
-        CU(launch_xround(p, true, st));
-        if (c->xfn(c->xuser, p.xbuf, (int64_t)B * p.xkmax * (p.DP + 2), st) != 0)
-          return fail(c, FMS_E_NCCL, "round exchange failed");
-        CU(launch_xround(p, false, st));
+      for (int s = 0; s < max_iters + c->poll; s += c->poll) {
+        for (int k = 0; k < c->poll; ++k) {
+          CU(launch_plan(p, st));
+          if (c->profile) {
+            const size_t slot = launches;
+            if (c->ev.size() < 2 * (slot + 1)) {
+              cudaEvent_t e0, e1;
+              CU(cudaEventCreate(&e0));
+              CU(cudaEventCreate(&e1));
+              c->ev.push_back(e0);
+              c->ev.push_back(e1);
+            }
+            if (c->h_prof_cap < slot + 1) {
+              size_t ncap = std::max<size_t>(256, 2 * (slot + 1));
+              int* np = nullptr;
+              CU(cudaMallocHost(&np, ncap * kProfInts * sizeof(int)));
+              if (c->h_prof) {
+                CU(cudaStreamSynchronize(st));
+                ++syncs;
+                memcpy(np, c->h_prof, c->h_prof_cap * kProfInts * sizeof(int));
+                cudaFreeHost(c->h_prof);
+              }
+              c->h_prof = np;
+              c->h_prof_cap = ncap;
+            }
+            CU(cudaEventRecord(c->ev[2 * slot], st));
+            CU(run_iter(p, tm, c->num_sms, st));
+            CU(cudaEventRecord(c->ev[2 * slot + 1], st));
+            CU(cudaMemcpyAsync(c->h_prof + slot * kProfInts, p.counters, kProfInts * sizeof(int), cudaMemcpyDeviceToHost,
+                               st));
+            ++launches;
+          } else {
+            CU(run_iter(p, tm, c->num_sms, st));
+          }
+          if (pshard && p.pkmax > 0) {  // window sums and counts over all pixels
+            CU(launch_pstep(p, true, st));
+            fms_status g = pxchg((size_t)B * p.pkmax * (2 * p.DP + 1), "step");
+            if (g != FMS_OK) return g;
+            CU(launch_pstep(p, false, st));
+            kernels += 2;
+          }
+          CU(launch_update(p, c->num_sms, st));
+          if (p.world > 1) {  // seed sharding: per-frame step counts summed over the ranks
+            CU(launch_xchg_pack(p, st));
+            if (c->xfn(c->xuser, p.xchg, (int64_t)B * 4, st) != 0) return fail(c, FMS_E_NCCL, "step exchange failed");
+          }
+          CU(launch_ctl(p, st));
+          ++steps;
+          kernels += p.world > 1 ? 5 : 4;  // plan, iter, update, (exchange pack), ctl_step
+        }
+        CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        ++syncs;
+        if (c->h_counters[5]) return fail(c, FMS_E_INTERNAL, "work-item capacity exceeded");
+        if (c->h_counters[3] == 0) break;  // no frame still iterating
+      }
+      if (p.world > 1) {  // seed sharding: every rank gets every owner's converged seeds before the merge
+        CU(launch_xkmax(p, st));
+        CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        ++syncs;
+        p.xkmax = c->h_counters[8];
+        if (p.xkmax > 0) {
+          CU(launch_xround(p, true, st));
+          if (c->xfn(c->xuser, p.xbuf, (int64_t)B * p.xkmax * (p.DP + 2), st) != 0)
+            return fail(c, FMS_E_NCCL, "round exchange failed");
+          CU(launch_xround(p, false, st));
+          kernels += 2;
+        }
+        kernels += 1;
+      }
+      CU(launch_post(p, tm, c->num_sms, st, !pshard));
+      kernels += 4;  // merge, assign (tensor cores), assign (CUDA cores, > 128 centres), osop
+      if (pshard) {  // histogram, candidate count and coverage over all pixels before the OSOP step
+        CU(launch_ppost(p, true, st));
+        fms_status g = pxchg(post_ints, "round");
+        if (g != FMS_OK) return g;
+        CU(launch_ppost(p, false, st));
+        CU(launch_osop(p, st));
         kernels += 2;
       }
+      CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+        ++syncs;
+      if (c->h_counters[2] == 0) break;  // every frame DONE (or in error)
+    }
+    if (cap > 0) {
+      CU(launch_output(p, centres, cap, st));
       kernels += 1;
     }
-    CU(launch_post(p, tm, c->num_sms, st, !pshard));
-    kernels += 4;  // merge, assign (tensor cores), assign (CUDA cores, > 256 centres), osop
-    if (pshard) {  // histogram, candidate count and coverage over all pixels before the OSOP step
-      CU(launch_ppost(p, true, st));
-      fms_status g = pxchg(post_ints, "round");
-      if (g != FMS_OK) return g;
-      CU(launch_ppost(p, false, st));
-      CU(launch_osop(p, st));
-      kernels += 2;
-    }
-    CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    if (c->h_counters[2] == 0) break;  // every frame DONE (or in error)
-  }
-  if (cap > 0) {
-    CU(launch_output(p, centres, cap, st));
-    kernels += 1;
   }
   CU(cudaEventRecord(c->t1, st));
   CU(cudaMemcpyAsync(c->h_ctl, p.ctl, sizeof(FrameCtl) * B, cudaMemcpyDeviceToHost, st));
+  if (gmode) CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  ++syncs;
   CU(cudaGetLastError());
+  if (gmode) {
+    if (c->h_counters[5]) return fail(c, FMS_E_INTERNAL, "work-item capacity exceeded");
+    if (c->h_counters[16]) return fail(c, FMS_E_INTERNAL, "device loop did not terminate");
+    steps = c->h_counters[14];
+    // prologue + per round (select 7, set_cond, merge/assign/assign/osop, round_cond) + per step
+    // (plan, K2, update, ctl, step_cond) + output
+    kernels = (p.metric == 1 ? 4 : 2) + 1 + (long long)c->h_counters[15] * 13 + (long long)steps * 5 + (cap > 0);
+  }
 
   fms_status result = FMS_OK;
   for (int f = 0; f < B; ++f) {
@@ -541,6 +684,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
     rs->workspace_bytes = (int64_t)c->ws_bytes;
     rs->steps = steps;
     rs->launches = kernels;
+    rs->host_syncs = syncs;
     if (c->profile) {
       for (int l = 0; l < launches; ++l) {
         const int* snap = c->h_prof + (size_t)l * kProfInts;
@@ -613,6 +757,13 @@ void fms_ctx_destroy(void* ctx) {
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->cstream) cudaStreamDestroy(c->cstream);
   for (auto e : c->ev) cudaEventDestroy(e);
+  for (auto& e : c->gcache) {
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+    if (e.graph) cudaGraphDestroy(e.graph);
+  }
+  for (int i = 0; i < 3; ++i)
+    if (c->gst[i]) cudaStreamDestroy(c->gst[i]);
+  if (c->h_io) cudaFreeHost(c->h_io);
   if (c->t0) cudaEventDestroy(c->t0);
   if (c->t1) cudaEventDestroy(c->t1);
   delete c;
@@ -684,6 +835,11 @@ fms_status fms_set_option(void* ctx, const char* key, int64_t value) {
   if (!strcmp(key, "kernel_profile")) {
     if (value < 0 || value > 1) return fail(c, FMS_E_INVALID, "kernel_profile must be 0 (flat) or 1 (Gaussian)");
     c->kprofile = (int)value;
+    return FMS_OK;
+  }
+  if (!strcmp(key, "graph")) {  // 1: device-resident loop (one CUDA graph launch per call); 0: host-polled
+    if (value < 0 || value > 1) return fail(c, FMS_E_INVALID, "graph must be 0 or 1");
+    c->use_graph = (int)value;
     return FMS_OK;
   }
   if (!strcmp(key, "poll_steps")) {  // a frame that finishes idles at most poll_steps - 1 steps
@@ -851,6 +1007,7 @@ fms_status fms_cluster_batch_host(void* ctx, const float* emb_host, int32_t B, i
     acc.iter_items += rs.iter_items;
     acc.launches += rs.launches;
     acc.iter_count_units += rs.iter_count_units;
+    acc.host_syncs += rs.host_syncs;
     CU(cudaEventRecord(c->ev_done, st));
     CU(cudaStreamWaitEvent(cs, c->ev_done, 0));
     CU(cudaMemcpyAsync(labels_host + (size_t)c_off[i] * n, d_lab, (size_t)Bi * n * 4, cudaMemcpyDeviceToHost, cs));

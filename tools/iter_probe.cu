@@ -76,7 +76,6 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   const double pairs = (double)T * 128 * n;
   for (int v : {0}) {
-    p.variant = v;
     for (int w = 0; w < 3; ++w) launch_iter(DP, tm, p, 148, 0);
     cudaEventRecord(e0);
     const int reps = 10;
@@ -94,7 +93,6 @@ int main(int argc, char** argv) {
            ms * 1e6 / tiles_per_sm, pairs * 64 / (ms * 1e-3) / 1e12);
   }
   // event timeline of CTA 0 for the full kernel
-  p.variant = argc > 4 ? atoi(argv[4]) : 256;
   launch_iter(DP, tm, p, 148, 0);
   cudaDeviceSynchronize();
   std::vector<long long> h(16 * 512 * 8);
