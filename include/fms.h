@@ -30,11 +30,12 @@ typedef enum {
   FMS_E_INVALID = 2,   /* usage: n<1, d<1 or d>32, h not in (0,1), tol<=0, max_iters<1, bad policy ("2") */
   FMS_E_ZERO_NORM = 3, /* a row has zero or non-finite norm: no direction (Eq. 9 needs |x|>0; "3") */
   FMS_E_STALLED = 4,   /* no seed converged in round 0 ("4") */
-  FMS_E_CAPACITY = 5,  /* K > centres_cap (labels still valid; *K_out = required K) or an internal capacity */
+  FMS_E_CAPACITY = 5,  /* K > centres_cap only: the frame finished, labels are valid, *K_out = the required K */
   FMS_E_CUDA = 6,      /* CUDA runtime / launch error; message in fms_last_error */
   FMS_E_NCCL = 7,      /* reserved for the multi-GPU paths */
   FMS_E_OOM = 8,       /* workspace allocation failed */
-  FMS_E_INTERNAL = 9   /* internal consistency check failed */
+  FMS_E_INTERNAL = 9   /* internal capacity (seed, centre or merge-pool workspace) or consistency check failed;
+                          the frame's results are not valid */
 } fms_status;
 
 typedef enum {

@@ -8,7 +8,7 @@
 //     step_cond <- 1
 //     WHILE step_cond:                                 lockstep step, Alg. 2 l.4-9
 //       plan -> K2 -> K3 update -> ctl_step -> step_cond_kernel
-//     K4 merge -> K5 assign -> K7 osop -> round_cond_kernel
+//     K4 merge (SMEM sort; IF some pool > 8192: global sort) -> K5 assign -> K7 osop -> round_cond
 //   output centres
 //
 // The conditions are the counters the host loop polled: counters[3] (frames still iterating after
@@ -42,6 +42,15 @@ __global__ void round_cond_kernel(cudaGraphConditionalHandle h, Params p) {
     more = false;
   }
   cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
+// the global-memory merge path runs only when some frame's pool exceeds the SMEM sort (k_post.cu)
+__global__ void big_merge_cond_kernel(cudaGraphConditionalHandle h, Params p) {
+  cudaGraphSetConditional(h, p.counters[18] > 8192 ? 1u : 0u);
+}
+cudaError_t launch_big_merge_cond(cudaGraphConditionalHandle h, const Params& p, cudaStream_t st) {
+  big_merge_cond_kernel<<<1, 1, 0, st>>>(h, p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_set_cond(cudaGraphConditionalHandle h, unsigned v, cudaStream_t st) {

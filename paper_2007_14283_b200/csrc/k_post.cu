@@ -40,7 +40,7 @@ __device__ int merge_assemble(const Params& p, int f, unsigned long long* keys, 
   const int K = c.K_r;
   const int P = Kc + c.n_conv;
   if (P > p.P_cap) {
-    if (threadIdx.x == 0) { c.status = 5; c.phase = PH_ERROR; }
+    if (threadIdx.x == 0) { c.status = 9; c.phase = PH_ERROR; }  // FMS_E_INTERNAL: pool capacity
     return -1;
   }
   float* pool = p.pool + (size_t)f * p.P_cap * DP;
@@ -156,17 +156,18 @@ __device__ void merge_nms(const Params& p, int f, const int* vals, int P, float*
   const int Kn = s_kept;
   for (int k = threadIdx.x; k < Kn && k < p.C_cap; k += blockDim.x) p.hist[(size_t)f * p.C_cap + k] = 0;
   if (threadIdx.x == 0) {
-    if (s_err) { c.status = 5; c.phase = PH_ERROR; }
+    if (s_err) { c.status = 9; c.phase = PH_ERROR; }  // FMS_E_INTERNAL: centre capacity C_cap
     c.Kc = Kn < p.C_cap ? Kn : p.C_cap;
     c.ncand = 0;
   }
 }
 
-// pools up to kMergeSm: one CTA per frame, bitonic sort of the keys in SMEM
+// pools up to kMergeSm: one CTA per frame, bitonic sort of the keys in SMEM (larger pools are left
+// to the global-memory path below)
 template <int DP>
 __global__ void __launch_bounds__(1024) merge_kernel(Params p) {
   const int f = blockIdx.x;
-  if (p.ctl[f].phase != PH_POST) return;
+  if (p.ctl[f].phase != PH_POST || p.ctl[f].Kc + p.ctl[f].n_conv > kMergeSm) return;
   extern __shared__ uint8_t dsm[];
   __shared__ int sm[33];
   int P2 = 1;
@@ -195,28 +196,29 @@ __global__ void __launch_bounds__(1024) merge_kernel(Params p) {
   merge_nms<DP>(p, f, vals, P, cand, cand + 32 * DP);
 }
 
-// larger pools (Alg. 1 merges a mode per pixel): keys in global memory, a CUB segmented radix sort
-// between the two kernels
+// larger pools (Alg. 1 merges a mode per pixel; late OSOP rounds of many-cell frames): keys in global
+// memory, a CUB segmented radix sort between the two kernels.  Each frame's segment is [f P_cap,
+// f P_cap + P) for a frame with P > kMergeSm and empty otherwise.
 template <int DP>
 __global__ void __launch_bounds__(1024) merge_pool_kernel(Params p) {
   const int f = blockIdx.x;
-  if (p.ctl[f].phase != PH_POST) {
-    for (int i = threadIdx.x; i < p.P_cap; i += blockDim.x) {
-      p.mkeys[(size_t)f * p.P_cap + i] = ~0ull;
-      p.mvals[(size_t)f * p.P_cap + i] = -1;
-    }
-    return;
+  const int P = p.ctl[f].Kc + p.ctl[f].n_conv;
+  const bool big = p.ctl[f].phase == PH_POST && P > kMergeSm;
+  if (threadIdx.x == 0) {
+    p.moffs[f] = f * p.P_cap;
+    p.moffs_end[f] = f * p.P_cap + (big ? P : 0);
   }
+  if (!big) return;
   __shared__ int sm[33];
-  const int P = merge_assemble<DP>(p, f, p.mkeys + (size_t)f * p.P_cap, p.mvals + (size_t)f * p.P_cap, p.P_cap, sm);
-  (void)P;  // P < 0: capacity error flagged (phase ERROR), the NMS kernel skips the frame
+  const int Pa = merge_assemble<DP>(p, f, p.mkeys + (size_t)f * p.P_cap, p.mvals + (size_t)f * p.P_cap, P, sm);
+  if (Pa < 0 && threadIdx.x == 0) p.moffs_end[f] = f * p.P_cap;  // capacity error flagged (phase ERROR)
 }
 
 template <int DP>
 __global__ void __launch_bounds__(1024) merge_nms_kernel(Params p) {
   const int f = blockIdx.x;
   FrameCtl& c = p.ctl[f];
-  if (c.phase != PH_POST) return;
+  if (c.phase != PH_POST || c.Kc + c.n_conv <= kMergeSm) return;
   __shared__ float cand[32 * DP];
   __shared__ float keptv[kKeptSm * DP];
   merge_nms<DP>(p, f, p.mvals_sorted + (size_t)f * p.P_cap, c.Kc + c.n_conv, cand, keptv);
@@ -347,7 +349,10 @@ __global__ void osop_kernel(Params p) {
   }
   int tot;
   block_excl_scan(not_done, sm, &tot);
-  if (threadIdx.x == 0) p.counters[2] = tot;
+  if (threadIdx.x == 0) {
+    p.counters[2] = tot;
+    p.counters[18] = 0;  // largest merge pool of the next round (ctl_step)
+  }
 }
 
 template <int DP>
@@ -388,35 +393,40 @@ size_t merge_sort_temp_bytes(const Params& p) {
   return bytes;
 }
 
-__global__ void merge_offsets_kernel(Params p) {
-  for (int f = threadIdx.x; f <= p.B; f += blockDim.x) p.moffs[f] = f * p.P_cap;
-}
 
 cudaError_t launch_osop(const Params& p, cudaStream_t st) {
   osop_kernel<<<1, 1024, 0, st>>>(p);
   return cudaGetLastError();
 }
 
-// merge + assignment (+ the OSOP step unless `osop` is false: pixel sharding sums the histogram
-// over the ranks first)
-cudaError_t launch_post(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st, bool osop) {
+// merge, small pools (P <= kMergeSm, SMEM sort) -- every call
+cudaError_t launch_merge_small(const Params& p, cudaStream_t st) {
+  const int sm = merge_smem_bytes(p.P_cap < kMergeSm ? p.P_cap : kMergeSm, p.DP);
+  if (p.DP == 16) merge_kernel<16><<<p.B, 1024, sm, st>>>(p);
+  else merge_kernel<32><<<p.B, 1024, sm, st>>>(p);
+  return cudaGetLastError();
+}
+
+// merge, large pools (global-memory sort) -- only when some frame's pool exceeds kMergeSm
+// (counters[18], the largest pool of the round, set by ctl_step)
+cudaError_t launch_merge_big(const Params& p, cudaStream_t st) {
+  if (p.P_cap <= kMergeSm) return cudaSuccess;
+  if (p.DP == 16) merge_pool_kernel<16><<<p.B, 1024, 0, st>>>(p);
+  else merge_pool_kernel<32><<<p.B, 1024, 0, st>>>(p);
+  size_t tb = p.msort_bytes;
+  cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairs(p.msort_temp, tb, p.mkeys, p.mkeys_sorted, p.mvals,
+                                                           p.mvals_sorted, (int)((size_t)p.B * p.P_cap), p.B,
+                                                           p.moffs, p.moffs_end, 0, 64, st);
+  if (e != cudaSuccess) return e;
+  if (p.DP == 16) merge_nms_kernel<16><<<p.B, 1024, 0, st>>>(p);
+  else merge_nms_kernel<32><<<p.B, 1024, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// assignment (+ the OSOP step unless `osop` is false: pixel sharding sums the histogram over the
+// ranks first)
+cudaError_t launch_assign_osop(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st, bool osop) {
   const dim3 ga(16, p.B);
-  if (p.P_cap <= kMergeSm) {
-    const int sm = merge_smem_bytes(p.P_cap, p.DP);
-    if (p.DP == 16) merge_kernel<16><<<p.B, 1024, sm, st>>>(p);
-    else merge_kernel<32><<<p.B, 1024, sm, st>>>(p);
-  } else {
-    if (p.DP == 16) merge_pool_kernel<16><<<p.B, 1024, 0, st>>>(p);
-    else merge_pool_kernel<32><<<p.B, 1024, 0, st>>>(p);
-    merge_offsets_kernel<<<1, 256, 0, st>>>(p);
-    size_t tb = p.msort_bytes;
-    cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairs(p.msort_temp, tb, p.mkeys, p.mkeys_sorted, p.mvals,
-                                                             p.mvals_sorted, (int)((size_t)p.B * p.P_cap), p.B,
-                                                             p.moffs, p.moffs + 1, 0, 64, st);
-    if (e != cudaSuccess) return e;
-    if (p.DP == 16) merge_nms_kernel<16><<<p.B, 1024, 0, st>>>(p);
-    else merge_nms_kernel<32><<<p.B, 1024, 0, st>>>(p);
-  }
   cudaError_t e = launch_assign_tc(p.DP, tm, p, num_sms, st);  // frames with <= 128 centres
   if (e != cudaSuccess) return e;
   if (p.DP == 16) assign_kernel<16><<<ga, 256, 0, st>>>(p);    // the rest

@@ -172,7 +172,7 @@ __global__ void sel_prepare_kernel(Params p) {
     Kreq = c.K_next;
   }
   long long K = Kreq < ncand ? Kreq : ncand;
-  if (K > p.S_cap) { c.status = 5 /*CAPACITY*/; c.phase = PH_ERROR; return; }
+  if (K > p.S_cap) { c.status = 9 /*FMS_E_INTERNAL: seed capacity*/; c.phase = PH_ERROR; return; }
   c.K_r = (int)K;
   c.sample_count = 0;
   c.kth = ~0ull;

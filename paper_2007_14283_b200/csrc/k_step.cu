@@ -236,6 +236,7 @@ __global__ void ctl_step_kernel(Params p) {
     // rows for the intensity pass (this rank's converged seeds; all of them without sharding)
     const int nloc = nconv > 0 ? compact_seeds<DP>(p, f, K, ST_CONV, sm) : 0;
     if (threadIdx.x == 0) {
+      atomicMax(&p.counters[18], c.Kc + nconv);  // merge pool size: picks the merge path (k_post.cu)
       c.round_iters[r] = c.t;
       c.round_conv[r] = nconv;
       c.round_disc[r] = K - nconv;

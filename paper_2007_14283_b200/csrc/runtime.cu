@@ -34,7 +34,10 @@ cudaError_t setup_iter8_attrs();
 cudaError_t launch_set_cond(cudaGraphConditionalHandle h, unsigned v, cudaStream_t st);
 cudaError_t launch_step_cond(cudaGraphConditionalHandle h, const Params& p, cudaStream_t st);
 cudaError_t launch_round_cond(cudaGraphConditionalHandle h, const Params& p, cudaStream_t st);
-cudaError_t launch_post(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st, bool osop);
+cudaError_t launch_big_merge_cond(cudaGraphConditionalHandle h, const Params& p, cudaStream_t st);
+cudaError_t launch_merge_small(const Params& p, cudaStream_t st);
+cudaError_t launch_merge_big(const Params& p, cudaStream_t st);
+cudaError_t launch_assign_osop(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st, bool osop);
 cudaError_t launch_osop(const Params& p, cudaStream_t st);
 cudaError_t launch_pstat(const Params& p, bool pack, cudaStream_t st);
 cudaError_t launch_psel_kmax(const Params& p, cudaStream_t st);
@@ -236,12 +239,13 @@ size_t carve(Params& p, uint8_t* base) {
   p.ctl = (FrameCtl*)take(B * sizeof(FrameCtl));
   p.fscale = (float*)take(B * 4);
   p.io = (const IoPtrs*)take(sizeof(IoPtrs));
-  if (p.P_cap > kMaxPcap) {  // merge pool sorted in global memory (Alg. 1)
+  if (p.P_cap > kMaxPcap) {  // merge pools above 8192 sorted in global memory
     p.mkeys = (unsigned long long*)take(B * (size_t)p.P_cap * 8);
     p.mkeys_sorted = (unsigned long long*)take(B * (size_t)p.P_cap * 8);
     p.mvals = (int*)take(B * (size_t)p.P_cap * 4);
     p.mvals_sorted = (int*)take(B * (size_t)p.P_cap * 4);
-    p.moffs = (int*)take((size_t)(B + 1) * 4);
+    p.moffs = (int*)take((size_t)B * 4);
+    p.moffs_end = (int*)take((size_t)B * 4);
     p.msort_bytes = merge_sort_temp_bytes(p);
     p.msort_temp = take(p.msort_bytes + 16);
   }
@@ -265,19 +269,21 @@ fms_status build_graph(Ctx* c, const Params& p, const TMaps& tm, int32_t cap, Ct
   const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
   // at the current capture position of `s`: a kernel setting the new condition to 1, then a WHILE
   // node on it; returns the node's body graph
-  auto add_while = [&](cudaStream_t s, cudaGraphConditionalHandle* h, cudaGraph_t* body) -> fms_status {
+  auto add_cond = [&](cudaStream_t s, cudaGraphConditionalHandle* h, cudaGraph_t* body,
+                      cudaGraphConditionalNodeType type) -> fms_status {
     cudaStreamCaptureStatus cs;
     cudaGraph_t g = nullptr;
     const cudaGraphNode_t* deps = nullptr;
     size_t ndeps = 0;
     CU(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &ndeps));
     CU(cudaGraphConditionalHandleCreate(h, g, 0, 0));
-    CU(launch_set_cond(*h, 1u, s));
+    if (type == cudaGraphCondTypeWhile) CU(launch_set_cond(*h, 1u, s));
+    else CU(launch_big_merge_cond(*h, p, s));
     CU(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &ndeps));
     cudaGraphNodeParams np{};
     np.type = cudaGraphNodeTypeConditional;
     np.conditional.handle = *h;
-    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.type = type;
     np.conditional.size = 1;
     cudaGraphNode_t node;
     CU(cudaGraphAddNode(&node, g, deps, ndeps, &np));
@@ -291,13 +297,13 @@ fms_status build_graph(Ctx* c, const Params& p, const TMaps& tm, int32_t cap, Ct
   fms_status r = [&]() -> fms_status {
     CU(cudaMemsetAsync(p.counters, 0, kCounters * 4, s0));
     CU(launch_prep(p, s0));
-    fms_status q = add_while(s0, &h_round, &round_body);
+    fms_status q = add_cond(s0, &h_round, &round_body, cudaGraphCondTypeWhile);
     if (q != FMS_OK) return q;
     // ---- round body: select, the step loop, merge / assign / OSOP ----
     CU(cudaStreamBeginCaptureToGraph(s1, round_body, nullptr, nullptr, 0, mode));
     q = [&]() -> fms_status {
       CU(launch_select(p, c->num_sms, s1));
-      fms_status q2 = add_while(s1, &h_step, &step_body);
+      fms_status q2 = add_cond(s1, &h_step, &step_body, cudaGraphCondTypeWhile);
       if (q2 != FMS_OK) return q2;
       // ---- step body ----
       CU(cudaStreamBeginCaptureToGraph(s2, step_body, nullptr, nullptr, 0, mode));
@@ -313,7 +319,20 @@ fms_status build_graph(Ctx* c, const Params& p, const TMaps& tm, int32_t cap, Ct
       const cudaError_t e2 = cudaStreamEndCapture(s2, &gdone);
       if (q2 != FMS_OK) return q2;
       CU(e2);
-      CU(launch_post(p, tm, c->num_sms, s1, true));
+      CU(launch_merge_small(p, s1));
+      if (p.P_cap > kMaxPcap) {  // IF some pool exceeds the SMEM sort: the global-memory merge
+        cudaGraphConditionalHandle h_big;
+        cudaGraph_t big_body = nullptr;
+        q2 = add_cond(s1, &h_big, &big_body, cudaGraphCondTypeIf);
+        if (q2 != FMS_OK) return q2;
+        CU(cudaStreamBeginCaptureToGraph(s2, big_body, nullptr, nullptr, 0, mode));
+        const cudaError_t eb = launch_merge_big(p, s2);
+        cudaGraph_t gb = nullptr;
+        const cudaError_t ee = cudaStreamEndCapture(s2, &gb);
+        CU(eb);
+        CU(ee);
+      }
+      CU(launch_assign_osop(p, tm, c->num_sms, s1, true));
       CU(launch_round_cond(h_round, p, s1));
       return FMS_OK;
     }();
@@ -380,10 +399,9 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   p.S_cap = (int)S;
   p.S_pad = (int)align_up((size_t)S, kBM);
   p.C_cap = (int)std::min<long long>(ng, 65536);
-  // the merge pool holds the previous centres plus one round's converged seeds: bounded by the SMEM
-  // sort for the seeding policies; Alg. 1 (every pixel a seed) merges n modes in global memory
-  p.P_cap = pol->kind == FMS_SEEDS_ALL ? (int)std::min<long long>((long long)p.C_cap + p.S_cap, INT32_MAX / 2)
-                                       : (int)std::min<long long>((long long)p.C_cap + p.S_cap, kMaxPcap);
+  // the merge pool holds the previous centres plus one round's converged seeds; pools above 8192 are
+  // sorted in global memory (Alg. 1 merges n modes; late OSOP rounds of many-cell frames)
+  p.P_cap = (int)std::min<long long>((long long)p.C_cap + p.S_cap, INT32_MAX / 2);
   p.tiles_cap = B * (p.S_pad / kBM);
   p.n_chunks = (p.n_ptiles + kChunkTiles - 1) / kChunkTiles;
   p.items_cap = p.tiles_cap * p.n_chunks;
@@ -604,7 +622,10 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
         }
         kernels += 1;
       }
-      CU(launch_post(p, tm, c->num_sms, st, !pshard));
+      CU(launch_merge_small(p, st));
+      // the global-memory merge only when a pool exceeds the SMEM sort (the last poll read counters[18])
+      if (p.P_cap > kMaxPcap && c->h_counters[18] > kMaxPcap) CU(launch_merge_big(p, st));
+      CU(launch_assign_osop(p, tm, c->num_sms, st, !pshard));
       kernels += 4;  // merge, assign (tensor cores), assign (CUDA cores, > 128 centres), osop
       if (pshard) {  // histogram, candidate count and coverage over all pixels before the OSOP step
         CU(launch_ppost(p, true, st));

@@ -54,6 +54,11 @@ def test_sampled_frames_match_oracle(batch, b):
     ro = oracle.cluster(f.emb, h=0.1, pol=opol)
     assert ro.status == 0
     assert ari(labels[b], ro.labels) >= 0.999
+    # the bench's FLOP basis: the run's own seed-iteration counts equal the oracle's
+    fs = st["frames"][b]
+    assert fs["seed_iters"] == ro.trace["seed_iters"]
+    assert fs["round_seed_iters"] == ro.trace["round_seed_iters"]
+    assert fs["round_K"] == ro.trace["round_K"] and fs["round_iters"] == ro.trace["round_iters"]
     big = np.nonzero(np.bincount(ro.labels, minlength=ro.K) >= min_instance_px(f.n))[0]
     assert match_centres(centres[b, :K[b]], ro.centres[big])[2].max() <= 1e-4
 

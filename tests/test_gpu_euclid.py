@@ -70,3 +70,17 @@ def test_euclid_rejections():
         ctx.cluster(torch.zeros((1, 100, 4), device="cuda"), h=1.0)
     with pytest.raises(fms.FmsError):
         ctx.set_option("metric", 5)
+
+
+def test_huge_bandwidth_is_one_cluster():
+    """a bandwidth hundreds of times the data scale used to overflow the fp16 threshold
+    column (NaN similarities, every seed stalled).  h~ is clamped at 2 (scaled points are < 1 apart
+    by 2), so every pixel is in every window: one cluster at the data mean, as in the oracle."""
+    X = _blobs(3, 60, 6, 0.1, 2.0, seed=9)
+    for h in (50.0, 1e6):
+        lg, cg, K, fr = _gpu(X, h, kind=0, n_seeds=8, has_background=0)
+        ro = oracle.cluster(X, h=h, pol=oracle.policy(kind=0, n_seeds=8, has_background=0,
+                                                       metric=oracle.METRIC_EUCLID))
+        assert ro.status == 0 and ro.K == 1 and K == 1
+        assert np.all(lg == 0)
+        assert np.abs(cg[0] - ro.centres[0]).max() <= 1e-4 * max(1.0, np.abs(ro.centres[0]).max())
