@@ -25,21 +25,24 @@
 
 namespace fms {
 
-constexpr int kAsgMaxN = 128;     // centres per frame handled here (one MMA N)
-constexpr int kAsgGroups = 4;     // epilogue groups (tile mod 4), one TMEM buffer of 128 columns each
 constexpr int kAsgEpiWarp0 = 2;
-constexpr int kAsgEpiThreads = kAsgGroups * 4 * 32;
-constexpr int kAsgThreads = kAsgEpiWarp0 * 32 + kAsgEpiThreads;
 
-template <int DP>
+// NMAX = the most centres a frame may have to be assigned by this instantiation (one MMA, N <= NMAX):
+// 128 (frames with 1..128 centres) or 256 (129..256, e.g. C4's ~200 cells); the CUDA-core kernel
+// (assign_kernel, k_post.cu) takes frames with more.  TMEM holds 512 / NMAX similarity buffers, one
+// per epilogue group of 4 warps.
+template <int DP, int NMAX>
 struct AsgCfg {
+  static constexpr int GROUPS = 512 / NMAX;               // epilogue groups (tile mod GROUPS)
+  static constexpr int EPI_THREADS = GROUPS * 4 * 32;
+  static constexpr int THREADS = kAsgEpiWarp0 * 32 + EPI_THREADS;
   static constexpr int ROW_B = DP * 2;
   static constexpr int TILE_B = kBN * ROW_B;              // one pixel tile, one limb
-  static constexpr int CEN_B = kAsgMaxN * ROW_B;          // one centre split
+  static constexpr int CEN_B = NMAX * ROW_B;              // one centre split
   static constexpr uint32_t LAYOUT = DP == 16 ? 6u : 4u;  // SWIZZLE_32B / SWIZZLE_64B
   static constexpr uint32_t SBO = 8 * ROW_B;
   static constexpr int STAGES = DP == 16 ? 8 : 5;
-  static constexpr int SMEM = 1024 + 2 * 3 * CEN_B + STAGES * 2 * TILE_B + 2 * kAsgMaxN * 4 + 1024;
+  static constexpr int SMEM = 1024 + 2 * 3 * CEN_B + STAGES * 2 * TILE_B + 2 * NMAX * 4 + 1024;
 };
 
 // byte offset of (row, 16-byte chunk) in a K-major tile with 32-byte (SW32) / 64-byte (SW64)
@@ -50,14 +53,17 @@ __device__ __forceinline__ uint32_t swz_off(int row, int chunk) {
   else return row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4);
 }
 
+template <int NMAX>
 __device__ __forceinline__ bool asg_frame_active(const Params& p, int f) {
   const FrameCtl& c = p.ctl[f];
-  return c.phase == PH_POST && c.Kc > 0 && c.Kc <= kAsgMaxN;
+  return c.phase == PH_POST && c.Kc > (NMAX == 128 ? 0 : 128) && c.Kc <= NMAX;
 }
 
-template <int DP>
-__global__ void __launch_bounds__(kAsgThreads, 1) assign_tc_kernel(const __grid_constant__ TMaps tm, Params p) {
-  using Cfg = AsgCfg<DP>;
+template <int DP, int NMAX>
+__global__ void __launch_bounds__(AsgCfg<DP, NMAX>::THREADS, 1)
+    assign_tc_kernel(const __grid_constant__ TMaps tm, Params p) {
+  using Cfg = AsgCfg<DP, NMAX>;
+  constexpr int kAsgMaxN = NMAX, kAsgGroups = Cfg::GROUPS, kAsgEpiThreads = Cfg::EPI_THREADS;
   const long long n_items = (long long)p.B * p.n_ptiles;
   const int i_begin = (int)((n_items * blockIdx.x) / gridDim.x);
   const int i_end = (int)((n_items * (blockIdx.x + 1)) / gridDim.x);
@@ -100,7 +106,7 @@ __global__ void __launch_bounds__(kAsgThreads, 1) assign_tc_kernel(const __grid_
     uint32_t sphase = 0;
     for (int item = i_begin, f = i_begin / p.n_ptiles, t = i_begin - f * p.n_ptiles; item < i_end;
          ++item, t = (t + 1 == p.n_ptiles) ? (++f, 0) : t + 1) {
-      if (f != act_f) { act_f = f; act_v = asg_frame_active(p, f); }
+      if (f != act_f) { act_f = f; act_v = asg_frame_active<NMAX>(p, f); }
       if (!act_v) continue;
       if (f != last_f) {
         // stage this frame's centre split into buffer fcount & 1 once its previous user is done
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(kAsgThreads, 1) assign_tc_kernel(const __grid_
     uint64_t dch = 0, dcs = 0, dcl = 0;
     for (int item = i_begin, f = i_begin / p.n_ptiles, t = i_begin - f * p.n_ptiles; item < i_end;
          ++item, t = (t + 1 == p.n_ptiles) ? (++f, 0) : t + 1) {
-      if (f != act_f) { act_f = f; act_v = asg_frame_active(p, f); }
+      if (f != act_f) { act_f = f; act_v = asg_frame_active<NMAX>(p, f); }
       if (!act_v) continue;
       if (f != last_f) {
         if (last_f >= 0) tc_commit_el(&c_empty[(fcount - 1) & 1]);  // previous frame's centres free
@@ -215,7 +221,7 @@ __global__ void __launch_bounds__(kAsgThreads, 1) assign_tc_kernel(const __grid_
     int n_act = 0;  // active items of this CTA before the current frame
     for (int f = i_begin / p.n_ptiles; (long long)f * p.n_ptiles < i_end; ++f) {
       const int s0 = max(i_begin, f * p.n_ptiles), s1 = min(i_end, (f + 1) * p.n_ptiles);
-      if (!asg_frame_active(p, f)) continue;
+      if (!asg_frame_active<NMAX>(p, f)) continue;
       ++fcount;
       const int Kc = p.ctl[f].Kc;
       for (int item = s0 + (((grp - n_act) % kAsgGroups) + kAsgGroups) % kAsgGroups; item < s1;
@@ -285,17 +291,25 @@ __global__ void __launch_bounds__(kAsgThreads, 1) assign_tc_kernel(const __grid_
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-int assign_tc_smem_bytes(int DP) { return DP == 16 ? AsgCfg<16>::SMEM : AsgCfg<32>::SMEM; }
-
 cudaError_t setup_assign_attrs() {
-  cudaError_t e = cudaFuncSetAttribute(assign_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, AsgCfg<16>::SMEM);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(assign_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, AsgCfg<32>::SMEM);
+  const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  cudaError_t e = cudaFuncSetAttribute(assign_tc_kernel<16, 128>, a, AsgCfg<16, 128>::SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(assign_tc_kernel<32, 128>, a, AsgCfg<32, 128>::SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(assign_tc_kernel<16, 256>, a, AsgCfg<16, 256>::SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(assign_tc_kernel<32, 256>, a, AsgCfg<32, 256>::SMEM);
+  return e;
 }
 
+// both tensor-core instantiations; a frame is assigned by the one whose centre range holds its Kc
+// (CTAs of the other exit after scanning their item range)
 cudaError_t launch_assign_tc(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st) {
-  if (DP == 16) assign_tc_kernel<16><<<grid, kAsgThreads, AsgCfg<16>::SMEM, st>>>(tm, p);
-  else assign_tc_kernel<32><<<grid, kAsgThreads, AsgCfg<32>::SMEM, st>>>(tm, p);
+  if (DP == 16) {
+    assign_tc_kernel<16, 128><<<grid, AsgCfg<16, 128>::THREADS, AsgCfg<16, 128>::SMEM, st>>>(tm, p);
+    if (p.C_cap > 128) assign_tc_kernel<16, 256><<<grid, AsgCfg<16, 256>::THREADS, AsgCfg<16, 256>::SMEM, st>>>(tm, p);
+  } else {
+    assign_tc_kernel<32, 128><<<grid, AsgCfg<32, 128>::THREADS, AsgCfg<32, 128>::SMEM, st>>>(tm, p);
+    if (p.C_cap > 128) assign_tc_kernel<32, 256><<<grid, AsgCfg<32, 256>::THREADS, AsgCfg<32, 256>::SMEM, st>>>(tm, p);
+  }
   return cudaGetLastError();
 }
 

@@ -48,7 +48,8 @@ namespace fms {
 namespace k8 {
 constexpr int kEpiWarps = 16;
 constexpr int kWarpTma = kEpiWarps, kWarpMma1 = kEpiWarps + 1, kWarpMma2 = kEpiWarps + 2;
-constexpr int kThreads = (kEpiWarps + 3) * 32;
+constexpr int kWarpTmaQ = kEpiWarps + 3;  // producer of the digit-plane ring
+constexpr int kThreads = (kEpiWarps + 4) * 32;
 }  // namespace k8
 
 template <int DP>
@@ -56,10 +57,13 @@ struct Iter8Cfg {
   // epilogue groups (tiles in flight): 4 groups of 4 warps for 16-lane rows; 32-lane rows keep 2
   // groups of 8 (their segment sums and pixel stages would not fit shared memory with 4)
 #ifdef K8_GROUPS
-  static constexpr int GROUPS = DP == 16 ? K8_GROUPS : 2;
+  static constexpr int GROUPS = K8_GROUPS;
 #else
-  static constexpr int GROUPS = DP == 16 ? 4 : 2;
+  static constexpr int GROUPS = 4;
 #endif
+  // 32-lane rows: a drain adds its sums straight to the global accumulator (fp64 atomics of exact
+  // integers) instead of shared-memory segment sums, which leaves room for a deeper pixel ring
+  static constexpr bool DIRECT = DP == 32;
   static constexpr int GROUP_WARPS = k8::kEpiWarps / GROUPS;  // a multiple of 4 (one per lane quarter)
   static constexpr int COLS_PER_WARP = kBN / (GROUP_WARPS / 4);
   static constexpr int PARTS = COLS_PER_WARP / 64;            // 64-column tcgen05.ld per part
@@ -70,31 +74,48 @@ struct Iter8Cfg {
   static constexpr uint32_t SBO = 8 * ROW_B;              // 8-row core-matrix group stride
   static constexpr int NQ = 3 * DP;                       // digit planes (= Gq columns)
   static constexpr int Q_B = NQ * kBN;                    // digit planes of one tile (128 B rows, SW128)
-  static constexpr int STAGE_B = 2 * TILE_B + Q_B;
+  static constexpr int L_B = 2 * TILE_B;                  // one stage of the limb ring (hi, lo)
 #ifdef K8_NC
   static constexpr int NC = K8_NC;
 #else
   static constexpr int NC = DP == 16 ? 3 : 2;             // C buffers
 #endif
+#ifdef K8_NP
+  static constexpr int NP = K8_NP;
+#else
   static constexpr int NP = DP == 16 ? (NC == 3 ? 2 : 3) : 3;  // P buffers (32 columns each)
+#endif
   static constexpr int P_COL = NC * kBN;
   static constexpr int G_COL = P_COL + NP * (kBN / 4);
   static_assert(G_COL + NQ <= 512, "TMEM budget");
-  static constexpr int STAGES = DP == 16 ? (GROUPS == 4 ? 9 : 11) : 4;
-  static constexpr int GS_B = kBM * DP * 8;               // int64 segment sums, [DP][kBM], per group
-  static constexpr int SMEM = 1024 + 6 * A_B + STAGES * STAGE_B + GROUPS * GS_B + 1024;
+  // Two rings: the limbs (MMA1's B operand) free a stage when MMA1 is done with it; the digit planes
+  // (MMA2's B) when MMA2 is.  A stage of the limb ring is held for a few hundred cycles, so the ring
+  // prefetches far ahead of the similarity MMAs for its size.
+  static constexpr int LSTAGES = DP == 16 ? 8 : 5;
+  static constexpr int QSTAGES = DP == 16 ? 10 : 8;
+  static constexpr int GS_B = DIRECT ? 0 : kBM * DP * 8;  // int64 segment sums, [DP][kBM], per group
+  static constexpr int SMEM = 1024 + 6 * A_B + LSTAGES * L_B + QSTAGES * Q_B + GROUPS * GS_B + 1024;
   static_assert(SMEM <= 232448, "shared memory");
-  static_assert(STAGE_B % 1024 == 0 && (2 * TILE_B) % 1024 == 0, "SW128 alignment of the digit planes");
+  static_assert(L_B % 1024 == 0 && Q_B % 1024 == 0, "SW128 alignment of the digit planes");
 };
 
-// chunk of pixel tiles per work item, chosen by plan_kernel for this launch
+// Work items: (frame f, chunk c of ct pixel tiles, seed tile j of f), ordered frame by frame, chunk by
+// chunk, and within a chunk over the frame's seed tiles.  A frame's pixels stream from HBM once per
+// step: the T_f seed tiles of a frame read the same chunk back to back (from L2), instead of each
+// seed tile streaming the whole frame (pixel tiles are 14 / 28 KB, far above the tensor work's
+// arithmetic intensity when every seed tile re-reads them from HBM).  Frame f's items are
+// [nch tile_off(f), nch (tile_off(f) + T_f)), so the tile task at item / nch belongs to f.
 struct Item8 {
   int f, tile, chunk, mode, key;  // key: frame * S_pad + tile * kBM (the segment a G drain belongs to)
 };
 __device__ __forceinline__ Item8 item8(const Params& p, int item, int nch) {
-  const int t = item / nch;
-  const TileTask tt = p.tiles[t];
-  return Item8{tt.f, tt.tile, item - t * nch, tt.mode, tt.f * p.S_pad + tt.tile * kBM};
+  const int f = p.tiles[item / nch].f;
+  const FrameCtl& c = p.ctl[f];
+  const int T = c.n_tiles_step;
+  const int L = item - nch * c.tile_off;
+  const int chunk = L / T;
+  const TileTask tt = p.tiles[c.tile_off + (L - chunk * T)];
+  return Item8{f, tt.tile, chunk, tt.mode, f * p.S_pad + tt.tile * kBM};
 }
 
 // two in-window differences per instruction: {c0 - tau_m, c1 - tau_m}
@@ -150,12 +171,15 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                    // [2 buffers][s_hi, s_hs, s_lo][A_B]
-  uint8_t* sX = smem + 6 * Cfg::A_B;                     // [STAGES][hi, lo, digit planes]
-  long long* gsm = reinterpret_cast<long long*>(sX + Cfg::STAGES * Cfg::STAGE_B);  // [group][DP][kBM]
+  uint8_t* sX = smem + 6 * Cfg::A_B;                     // [LSTAGES][hi, lo]
+  uint8_t* sQ = sX + Cfg::LSTAGES * Cfg::L_B;            // [QSTAGES][digit planes]
+  long long* gsm = reinterpret_cast<long long*>(sQ + Cfg::QSTAGES * Cfg::Q_B);  // [group][DP][kBM]
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(gsm) + kGroups * Cfg::GS_B);
-  uint64_t* x_full = bars;                    // [STAGES] pixel tile landed
-  uint64_t* x_empty = x_full + Cfg::STAGES;   // [STAGES] tile's weighted sum done: stage and P free
-  uint64_t* a_full = x_empty + Cfg::STAGES;   // [2] seed tile landed
+  uint64_t* x_full = bars;                    // [LSTAGES] limbs of a pixel tile landed
+  uint64_t* x_empty = x_full + Cfg::LSTAGES;  // [LSTAGES] the tile's similarity MMAs done
+  uint64_t* q_full = x_empty + Cfg::LSTAGES;  // [QSTAGES] digit planes landed
+  uint64_t* q_empty = q_full + Cfg::QSTAGES;  // [QSTAGES] the tile's weighted sum done: stage and P free
+  uint64_t* a_full = q_empty + Cfg::QSTAGES;  // [2] seed tile landed
   uint64_t* a_empty = a_full + 2;             // [2] seed tile consumed
   // similarity ready: one barrier per epilogue GROUP (not per C buffer), so that a group never waits
   // on a barrier whose previous phase is still pending (a waiter two phases ahead would see the
@@ -168,13 +192,15 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
   uint64_t* g_empty = g_full + kGroups;       // [1] Gq drained
   uint64_t* p_full = g_empty + 1;             // [NP] weights written
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(p_full + Cfg::NP);
-  static_assert((Cfg::STAGES * 2 + 5 + 2 * kGroups + Cfg::NC + Cfg::NP) * 8 + 4 <= 1024, "barrier area");
+  static_assert((Cfg::LSTAGES * 2 + Cfg::QSTAGES * 2 + 5 + 2 * kGroups + Cfg::NC + Cfg::NP) * 8 + 4 <= 1024,
+                "barrier area");
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
+    for (int i = 0; i < Cfg::LSTAGES; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
+    for (int i = 0; i < Cfg::QSTAGES; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < kGroups; ++i) mbar_init(&g_full[i], 1);
     mbar_init(g_empty, 4);  // drained by 4 warps (one per lane quarter)
@@ -185,9 +211,10 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
     fence_proxy_async();
   }
   if (warp == kWarpTma && lane == 0) {
-    tma_prefetch(&tm.xh); tma_prefetch(&tm.xl); tma_prefetch(&tm.xq);
+    tma_prefetch(&tm.xh); tma_prefetch(&tm.xl);
     tma_prefetch(&tm.sh); tma_prefetch(&tm.ss); tma_prefetch(&tm.sl);
   }
+  if (warp == kWarpTmaQ && lane == 0) tma_prefetch(&tm.xq);
   if (warp == kWarpMma1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
@@ -218,20 +245,42 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
         mbar_wait(&x_empty[stage], sphase ^ 1);
         K8_TL(0, xi, 0);
         if (lane == 0) {
-          uint8_t* st = sX + stage * Cfg::STAGE_B;
+          uint8_t* st = sX + stage * Cfg::L_B;
           const int xrow = (int)((tile0 + j) * kBN);
           if (K8_SKIP(32)) {
             mbar_arrive(&x_full[stage]);
           } else {
-            mbar_expect_tx(&x_full[stage], Cfg::STAGE_B);
+            mbar_expect_tx(&x_full[stage], Cfg::L_B);
             tma_load_2d(st, &tm.xh, &x_full[stage], 0, xrow);
             tma_load_2d(st + Cfg::TILE_B, &tm.xl, &x_full[stage], 0, xrow);
-            tma_load_2d(st + 2 * Cfg::TILE_B, &tm.xq, &x_full[stage], 0, (int)((tile0 + j) * Cfg::NQ));
           }
         }
         __syncwarp();
         ++xi;
-        if (++stage == Cfg::STAGES) { stage = 0; sphase ^= 1; }
+        if (++stage == Cfg::LSTAGES) { stage = 0; sphase ^= 1; }
+      }
+    }
+  } else if (warp == kWarpTmaQ) {
+    // ====================== TMA producer of the digit planes ======================
+    int stage = 0;
+    uint32_t sphase = 0;
+    for (int item = i_begin; item < i_end; ++item) {
+      const Item8 w = item8(p, item, nch);
+      const int cbeg = w.chunk * ct;
+      const int ccnt = min(ct, p.n_ptiles - cbeg);
+      const long long tile0 = (long long)w.f * p.n_ptiles + cbeg;
+      for (int j = 0; j < ccnt; ++j) {
+        mbar_wait(&q_empty[stage], sphase ^ 1);
+        if (lane == 0) {
+          if (K8_SKIP(32)) {
+            mbar_arrive(&q_full[stage]);
+          } else {
+            mbar_expect_tx(&q_full[stage], Cfg::Q_B);
+            tma_load_2d(sQ + stage * Cfg::Q_B, &tm.xq, &q_full[stage], 0, (int)((tile0 + j) * Cfg::NQ));
+          }
+        }
+        __syncwarp();
+        if (++stage == Cfg::QSTAGES) { stage = 0; sphase ^= 1; }
       }
     }
   } else if (warp == kWarpMma1) {
@@ -258,7 +307,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
         mbar_wait(&x_full[stage], sphase);
         K8_TL(1, i, 2);
         tc_fence_after();
-        const uint64_t dxh = dx0 + (uint64_t)(stage * (Cfg::STAGE_B >> 4));
+        const uint64_t dxh = dx0 + (uint64_t)(stage * (Cfg::L_B >> 4));
         const uint64_t dxl = dxh + (Cfg::TILE_B >> 4);
         const uint32_t d = tmem + buf * kBN;
         if (!K8_SKIP(2)) {
@@ -273,8 +322,9 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
             mma_ss_f16_el(d, dal + kk * 2, dxh + kk * 2, IDESC1, 1u);
         }
         tc_commit_el(&c_full[i % kGroups]);
+        tc_commit_el(&x_empty[stage]);  // the limbs stage is free once these MMAs complete
         K8_TL(1, i, 3);
-        if (++stage == Cfg::STAGES) { stage = 0; sphase ^= 1; }
+        if (++stage == Cfg::LSTAGES) { stage = 0; sphase ^= 1; }
       }
       tc_commit_el(&a_empty[ab]);  // seed tile free once this item's MMA1s complete
     }
@@ -283,8 +333,9 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
     // Gq (+)= P[i % NP] . Q once the epilogue group has written the weights (p_full); one commit frees
     // the pixel stage and with it the weight buffer (x_empty); at the end of an item hands Gq over.
     constexpr uint32_t IDESC2 = idesc_i8(kBM, Cfg::NQ);
-    const uint64_t dq0 = umma_desc(smem_u32(sX + 2 * Cfg::TILE_B), 16, 1024, 2);  // K-major SW128
+    const uint64_t dq0 = umma_desc(smem_u32(sQ), 16, 1024, 2);  // K-major SW128
     int stage = 0;
+    uint32_t sphase = 0;
     int i = 0;
     const uint32_t g_tmem = tmem + Cfg::G_COL;
     for (int item = i_begin, it = 0; item < i_end; ++item, ++it) {
@@ -296,18 +347,19 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
         const uint32_t pb = i % Cfg::NP;
         K8_TL(2, i, 0);
         mbar_wait(&p_full[pb], (i / Cfg::NP) & 1);
+        mbar_wait(&q_full[stage], sphase);
         K8_TL(2, i, 1);
         tc_fence_after();
         if (w.mode == 0 && !K8_SKIP(1)) {
-          const uint64_t bq = dq0 + (uint64_t)(stage * (Cfg::STAGE_B >> 4));
+          const uint64_t bq = dq0 + (uint64_t)(stage * (Cfg::Q_B >> 4));
           const uint32_t pa = tmem + Cfg::P_COL + pb * (kBN / 4);
 #pragma unroll
           for (int k = 0; k < kBN / 32; ++k)  // 32 pixels = 8 columns of packed u8 weights
             mma_ts_i8_el(g_tmem, pa + k * 8, bq + (uint64_t)(k * 2), IDESC2, (j == 0 && k == 0) ? 0u : 1u);
         }
-        tc_commit_el(&x_empty[stage]);  // pixel stage and weight buffer pb free once these complete
+        tc_commit_el(&q_empty[stage]);  // digit stage and weight buffer pb free once these complete
         K8_TL(2, i, 2);
-        if (++stage == Cfg::STAGES) stage = 0;
+        if (++stage == Cfg::QSTAGES) { stage = 0; sphase ^= 1; }
       }
       tc_commit_el(&g_full[(i - 1) % kGroups]);  // the group that handled the item's last tile drains
     }
@@ -322,18 +374,18 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     // tau_m = the float just below 2^11 tau (C is scaled by 2^11, exactly)
     const float tau_m = __uint_as_float(__float_as_uint(p.tau_f * kLimb) - 1u);
-    uint32_t ctile = 0;                               // running tile index over the CTA's stream
+    uint32_t tcur = 0;                                // running tile index over the CTA's stream
     uint32_t mine = 0;                                // tiles handled by this group so far
     long long* gs = gsm + (size_t)grp * (DP * kBM) + row;  // this group's segment sums of this row, [k][kBM]
     int seg = -1;                                     // segment (frame, seed tile) held in gs
     int seg_f = 0, seg_tile = 0;
     uint32_t drains = 0;                              // items this group has drained
-    if (h == 0) {
+    if (h == 0 && !Cfg::DIRECT) {
 #pragma unroll
       for (int k = 0; k < DP; ++k) gs[k * kBM] = 0;
     }
     auto flush = [&]() {
-      if (seg < 0) return;
+      if (Cfg::DIRECT || seg < 0) return;
       double* dst = p.gacc + ((size_t)seg_f * p.S_pad + (size_t)seg_tile * kBM + row) * DP;
 #pragma unroll
       for (int k = 0; k < DP; ++k) {
@@ -348,9 +400,10 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
       const int ccnt = min(ct, p.n_ptiles - w.chunk * ct);
       // the tile range of this item in the CTA's stream: [ctile, ctile + ccnt); this group's tiles
       // are those with index % kGroups == grp; the group owning the item's last tile drains its Gq
-      const uint32_t last_tile = ctile + (uint32_t)ccnt - 1;
-      for (int j = 0; j < ccnt; ++j, ++ctile) {
-        if ((int)(ctile % kGroups) != grp) continue;
+      const uint32_t base = tcur;
+      const uint32_t last_tile = base + (uint32_t)ccnt - 1;
+      const uint32_t first = base + (uint32_t)((grp - (int)(base % kGroups) + kGroups) % kGroups);
+      for (uint32_t ctile = first; ctile <= last_tile; ctile += kGroups) {  // this group's tiles only
         const uint32_t cb = ctile % Cfg::NC;
         const uint32_t pb = ctile % Cfg::NP;
         const int role = 3 + (grp * kGroupWarps + (warp % kGroupWarps)) % 16;
@@ -382,7 +435,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
             __syncwarp();
             if (lane == 0) mbar_arrive(&c_empty[cb]);  // MMA1 may overwrite C[cb]
           }
-          if (!p_free) p_free = mbar_test(&x_empty[u % Cfg::STAGES], (u / Cfg::STAGES) & 1);
+          if (!p_free) p_free = mbar_test(&q_empty[u % Cfg::QSTAGES], (u / Cfg::QSTAGES) & 1);
           uint32_t pk[16];
           if (!K8_SKIP(8)) {
 #pragma unroll
@@ -398,7 +451,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
           }
           K8_TL(role, ctile, 3);
           if (!p_free) {
-            mbar_wait(&x_empty[u % Cfg::STAGES], (u / Cfg::STAGES) & 1);
+            mbar_wait(&q_empty[u % Cfg::QSTAGES], (u / Cfg::QSTAGES) & 1);
             p_free = true;
           }
           K8_TL(role, ctile, 4);
@@ -427,7 +480,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
           K8_TL(role, ctile, 6);
           tc_fence_after();
           if (w.mode == 0) {
-            if (seg != w.key) {
+            if (!Cfg::DIRECT && seg != w.key) {
               flush();
               seg = w.key;
               seg_f = w.f;
@@ -445,7 +498,13 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
               for (int k = 0; k < 16; ++k) {
                 const long long s = (long long)(int)ga[k] * 65536ll + (long long)(int)gb[k] * 256ll + (int)gc[k];
                 // s = 255 x (an integer below 2^43): the correctly rounded product is within 1e-3 of it
-                gs[(k0 + k) * kBM] += __double2ll_rn((double)s * (1.0 / 255.0));
+                const long long v = __double2ll_rn((double)s * (1.0 / 255.0));
+                if constexpr (Cfg::DIRECT) {
+                  if (v != 0)
+                    atomicAdd(p.gacc + ((size_t)w.f * p.S_pad + (size_t)w.tile * kBM + row) * DP + k0 + k, (double)v);
+                } else {
+                  gs[(k0 + k) * kBM] += v;
+                }
               }
             }
           }
@@ -455,8 +514,9 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
           K8_TL(role, ctile, 7);
         }
       }
-      // count pass: each warp flushes its window counts when the segment ends
-      const bool last = (item + 1 == i_end) || ((item + 1) / nch != item / nch);
+      tcur = base + (uint32_t)ccnt;
+      // count pass: each warp flushes its window counts when the segment (same seed tile) ends
+      const bool last = (item + 1 == i_end) || item8(p, item + 1, nch).key != w.key;
       if (last && w.mode != 0) {
         if (cnt) atomicAdd(p.cacc + (size_t)w.f * p.S_pad + (size_t)w.tile * kBM + row, cnt >> 3);
         cnt = 0;

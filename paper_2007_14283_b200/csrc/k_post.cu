@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(256) assign_kernel(Params p) {
   // covered by a block-stride loop over 256-pixel blocks
   const int f = blockIdx.y;
   FrameCtl& c = p.ctl[f];
-  if (c.phase != PH_POST || (c.Kc > 0 && c.Kc <= 128)) return;  // <= 128 centres: assign_tc_kernel
+  if (c.phase != PH_POST || (c.Kc > 0 && c.Kc <= 256)) return;  // <= 256 centres: assign_tc_kernel
   const int nb = (int)((p.n + 255) / 256);
   for (int bid = blockIdx.x; bid < nb; bid += gridDim.x) {
   const int Kc = c.Kc;
@@ -427,7 +427,7 @@ cudaError_t launch_merge_big(const Params& p, cudaStream_t st) {
 // ranks first)
 cudaError_t launch_assign_osop(const Params& p, const TMaps& tm, int num_sms, cudaStream_t st, bool osop) {
   const dim3 ga(16, p.B);
-  cudaError_t e = launch_assign_tc(p.DP, tm, p, num_sms, st);  // frames with <= 128 centres
+  cudaError_t e = launch_assign_tc(p.DP, tm, p, num_sms, st);  // frames with <= 256 centres
   if (e != cudaSuccess) return e;
   if (p.DP == 16) assign_kernel<16><<<ga, 256, 0, st>>>(p);    // the rest
   else assign_kernel<32><<<ga, 256, 0, st>>>(p);

@@ -70,7 +70,8 @@ __global__ void plan_kernel(Params p) {
     int ct = kChunkTiles, nch = p.n_chunks;
     if (p.profile == 0) {
       const long long want = (long long)s_tiles_total * p.n_ptiles / (8ll * p.num_sms);
-      ct = (int)(want < 1 ? 1 : (want > kChunkMax ? kChunkMax : want));
+      const long long cmax = p.DP == 16 ? kChunkMax : kChunkMax / 2;  // 28 KB tiles at DP = 32
+      ct = (int)(want < 1 ? 1 : (want > cmax ? cmax : want));
       if (ct > p.n_ptiles) ct = p.n_ptiles;
       nch = (p.n_ptiles + ct - 1) / ct;
     }

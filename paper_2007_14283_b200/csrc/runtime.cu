@@ -626,7 +626,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
       // the global-memory merge only when a pool exceeds the SMEM sort (the last poll read counters[18])
       if (p.P_cap > kMaxPcap && c->h_counters[18] > kMaxPcap) CU(launch_merge_big(p, st));
       CU(launch_assign_osop(p, tm, c->num_sms, st, !pshard));
-      kernels += 4;  // merge, assign (tensor cores), assign (CUDA cores, > 128 centres), osop
+      kernels += 5;  // merge, assign (tensor cores, <= 128 and <= 256 centres), assign (CUDA cores), osop
       if (pshard) {  // histogram, candidate count and coverage over all pixels before the OSOP step
         CU(launch_ppost(p, true, st));
         fms_status g = pxchg(post_ints, "round");
@@ -655,9 +655,9 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
     if (c->h_counters[5]) return fail(c, FMS_E_INTERNAL, "work-item capacity exceeded");
     if (c->h_counters[16]) return fail(c, FMS_E_INTERNAL, "device loop did not terminate");
     steps = c->h_counters[14];
-    // prologue + per round (select 7, set_cond, merge/assign/assign/osop, round_cond) + per step
+    // prologue + per round (select 7, set_cond, merge, 3 assign, osop, round_cond) + per step
     // (plan, K2, update, ctl, step_cond) + output
-    kernels = (p.metric == 1 ? 4 : 2) + 1 + (long long)c->h_counters[15] * 13 + (long long)steps * 5 + (cap > 0);
+    kernels = (p.metric == 1 ? 4 : 2) + 1 + (long long)c->h_counters[15] * 14 + (long long)steps * 5 + (cap > 0);
   }
 
   fms_status result = FMS_OK;

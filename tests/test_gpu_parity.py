@@ -225,11 +225,19 @@ def _many_clusters(k=200, per=80, d=16, seed=7):
 
 
 def test_more_than_128_modes_exact():
-    """> 128 modes: the last rounds' assignment runs on the CUDA-core kernel, earlier ones on the
-    tensor cores -- both must reproduce the oracle exactly (Alg. 2 l.12-14)."""
+    """129..256 modes: the last rounds' assignment runs on the N = 256 tensor-core instantiation,
+    earlier ones on the N = 128 one -- both must reproduce the oracle exactly (Alg. 2 l.12-14,
+    P:204-206)."""
     emb = _many_clusters()
     lg, cg, Kg, st, ro = check_exact(emb, rng_seed=3, has_background=0)
     assert ro.K > 128 and max(ro.trace["round_Kc"]) > 128
+
+
+def test_more_than_256_modes_exact():
+    """> 256 modes: the CUDA-core assignment kernel (assign_kernel) -- exact vs the oracle."""
+    emb = _many_clusters(k=300, per=40, seed=11)
+    lg, cg, Kg, st, ro = check_exact(emb, rng_seed=3, has_background=0)
+    assert ro.K > 256 and max(ro.trace["round_Kc"]) > 256
 
 
 def test_c5_small_stack_ari():

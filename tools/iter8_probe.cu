@@ -8,6 +8,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "fms_device.cuh"
@@ -109,6 +110,10 @@ int main(int argc, char** argv) {
   for (int t = 0; t < T; ++t) tt[t] = TileTask{t / T_per_frame, t % T_per_frame, 0, 0, 0, 0, 0, 0};
   cudaMalloc(&p.tiles, T * sizeof(TileTask));
   cudaMemcpy(p.tiles, tt.data(), T * sizeof(TileTask), cudaMemcpyHostToDevice);
+  std::vector<FrameCtl> hc(B);
+  for (int f = 0; f < B; ++f) { memset(&hc[f], 0, sizeof(FrameCtl)); hc[f].tile_off = f * T_per_frame; hc[f].n_tiles_step = T_per_frame; }
+  cudaMalloc(&p.ctl, B * sizeof(FrameCtl));
+  cudaMemcpy(p.ctl, hc.data(), B * sizeof(FrameCtl), cudaMemcpyHostToDevice);
   cudaMalloc(&p.counters, 64 * 4);
   cudaMalloc(&p.gacc, (size_t)B * S_pad * DP * 8);
   cudaMalloc(&p.cacc, (size_t)B * S_pad * 4);
@@ -127,7 +132,7 @@ int main(int argc, char** argv) {
   const double pairs = (double)T * 128 * n;
   {
     // barrier offsets (relative to the 1024-aligned dynamic smem base) for decoding stuck waits
-    const int S = DP == 16 ? 11 : 5;
+    const int S = DP == 16 ? 9 : 6;
     const int stage_b = 2 * 128 * DP * 2 + 3 * DP * 128;
     const int bars = 6 * 128 * DP * 2 + S * stage_b + 128 * DP * 8;
     printf("barriers at smem+0x%x: x_full[%d], x_empty[%d], a_full[2], a_empty[2], c_full[NC], c_empty[NC], g_full, "
