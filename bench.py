@@ -153,7 +153,7 @@ def measured_peaks():
 def ncu_traffic():
     """dram bytes per K2 launch from the committed ncu --set full summary, if present."""
     try:
-        with open(os.path.join(ROOT, "profiles", "iter_kernel_ncu.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "k2_ncu.json")) as f:
             return json.load(f).get("dram_bytes_per_launch")
     except Exception:
         return None

@@ -65,6 +65,8 @@ struct Iter8Cfg {
   // integers) instead of shared-memory segment sums, which leaves room for a deeper pixel ring
   static constexpr bool DIRECT = DP == 32;
   static constexpr int GROUP_WARPS = k8::kEpiWarps / GROUPS;  // a multiple of 4 (one per lane quarter)
+  // (2 groups of 8 warps hung in a probe run at DP = 16 and is not used; 4 is the tested layout)
+  static_assert(GROUPS == 4, "epilogue layout: 4 groups of 4 warps");
   static constexpr int COLS_PER_WARP = kBN / (GROUP_WARPS / 4);
   static constexpr int PARTS = COLS_PER_WARP / 64;            // 64-column tcgen05.ld per part
   static constexpr int ROW_B = DP * 2;                    // bytes per fp16 row

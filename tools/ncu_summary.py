@@ -71,7 +71,17 @@ def full(src, dst, idx=0):
         mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u.get(k, "byte"), 1)
         return v * mult
 
-    dur_us = f("gpu__time_duration.sum") * (1e-3 if u.get("gpu__time_duration.sum") == "nsecond" else 1.0)
+    def stalls():
+        st = []
+        for k in hdr:
+            if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
+                v = f(k)
+                if v:
+                    st.append((k[len("smsp__pcsamp_warps_issue_stalled_"):], v))
+        tot = sum(v for _, v in st) or 1.0
+        return {k: round(100 * v / tot, 1) for k, v in sorted(st, key=lambda x: -x[1])[:6]}
+
+    dur_us = f("gpu__time_duration.sum") * UNIT.get(u.get("gpu__time_duration.sum", "usecond"), 1.0)
     rd, wr = bytes_("dram__bytes_read.sum"), bytes_("dram__bytes_write.sum")
     summary = {
         "kernel": d.get("Kernel Name", ""),
@@ -85,6 +95,12 @@ def full(src, dst, idx=0):
         "tensor_pipe_cycles_active_pct_of_peak_elapsed": f("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
         "fp16_tensor_ops_pct_of_peak_elapsed": f("sm__ops_path_tensor_src_fp16_dst_fp32.avg.pct_of_peak_sustained_elapsed"),
         "issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+        "hmma_subpipe_active_pct_of_peak_active": f("sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active"),
+        "imma_subpipe_active_pct_of_peak_active": f("sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active"),
+        "dram_read_tb_s": (rd / (dur_us * 1e-6) / 1e12) if rd and dur_us else None,
+        "dram_read_pct_of_peak_elapsed": f("dram__bytes_read.sum.pct_of_peak_sustained_elapsed"),
+        "l1tex_throughput_pct_of_peak_elapsed": f("l1tex__throughput.avg.pct_of_peak_sustained_elapsed"),
+        "warp_stall_top": stalls(),
         "l2_hit_rate_pct": f("lts__t_sector_hit_rate.pct"),
         "registers_per_thread": f("launch__registers_per_thread"),
         "threads_per_block": f("launch__block_size"),
