@@ -131,6 +131,32 @@ void fms_session_destroy(void* session);
 typedef int (*fms_exchange_fn)(void* user, int32_t* buf, int64_t count, void* stream);
 fms_status fms_set_exchange(void* ctx, fms_exchange_fn fn, void* user, int32_t rank, int32_t world);
 
+/* Seed sharding's per-round exchange as an all-gather (optional, SURVEY.md 8(e)2 "one allgather per
+ * OSOP round of ... mode slots"): with fn set and seed sharding on, every rank packs only the seeds it
+ * owns (j % world == rank, packed at row j / world) and `fn` must gather the ranks' int32 device
+ * buffers: recv[r * count .. (r + 1) * count) = send of rank r, stream-ordered on `stream`, returning
+ * 0 on success -- each rank sends 1/world of the round's rows instead of all-reducing a zero-padded
+ * copy of all of them.  fn = NULL restores the all-reduce exchange.  A nonzero return fails the
+ * clustering call with FMS_E_NCCL. */
+typedef int (*fms_allgather_fn)(void* user, const int32_t* send, int32_t* recv, int64_t count, void* stream);
+fms_status fms_set_allgather(void* ctx, fms_allgather_fn fn, void* user);
+
+/* In-library NCCL (SURVEY.md 8(b) fms_ctx_create_dist): the sharding collectives run as NCCL calls
+ * from inside the library on its stream -- no callback into the caller per lockstep step.
+ * fms_nccl_unique_id writes a 128-byte ncclUniqueId (rank 0 calls it and shares the bytes, e.g.
+ * through torch.distributed); every rank then calls fms_set_nccl (collective: blocks until all `world`
+ * ranks joined) with mode FMS_SHARD_SEEDS (per-step counts by ncclAllReduce, per-round owned rows by
+ * ncclAllGather) or FMS_SHARD_PIXELS (every exchange by ncclAllReduce; n_global / offset as in
+ * fms_set_pixel_shard).  libnccl.so.2 is opened at run time (FMS_E_NCCL if it cannot be, or on an NCCL
+ * error; the message names it).  One GPU per rank.  world = 1 turns sharding off.
+ * fms_ctx_create_dist = fms_ctx_create + fms_set_nccl. */
+enum { FMS_SHARD_SEEDS = 1, FMS_SHARD_PIXELS = 2 };
+fms_status fms_nccl_unique_id(void* id_out);
+fms_status fms_set_nccl(void* ctx, const void* unique_id, int32_t rank, int32_t world, int32_t mode,
+                        int64_t n_global, int64_t offset);
+fms_status fms_ctx_create_dist(void** ctx_out, int device, const void* unique_id, int32_t rank, int32_t world,
+                               int32_t mode, int64_t n_global, int64_t offset);
+
 /* Pixel sharding (for frames or stacks too large for one GPU).  Every window sum of
  * the lockstep iteration is a sum over pixels (Eq. 8 gated by Eq. 11, Alg. 2 l.4-9, PAPER.md
  * P:137-139), and so are the mode intensities, the label histogram that feeds I and r of

@@ -16,10 +16,14 @@ STATUS = {0: "OK", 2: "INVALID", 3: "ZERO_NORM", 4: "STALLED", 5: "CAPACITY", 6:
           9: "INTERNAL"}
 EXPORTS = ["fms_default_policy", "fms_ctx_create", "fms_ctx_destroy", "fms_last_error", "fms_version",
            "fms_set_option", "fms_set_exchange", "fms_set_pixel_shard", "fms_cluster", "fms_cluster_batch", "fms_cluster_batch_host",
-           "fms_session_create", "fms_session_step", "fms_session_seeds", "fms_session_destroy"]
+           "fms_session_create", "fms_session_step", "fms_session_seeds", "fms_session_destroy",
+           "fms_set_allgather", "fms_nccl_unique_id", "fms_set_nccl", "fms_ctx_create_dist"]
+SHARD_SEEDS, SHARD_PIXELS = 1, 2
 
 # int (*)(void* user, int32_t* buf, int64_t count, void* stream): in-place int32 sum over ranks
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+# int (*)(void* user, const int32_t* send, int32_t* recv, int64_t count, void* stream): all-gather
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfms.so")
@@ -84,6 +88,10 @@ def lib() -> C.CDLL:
         L.fms_set_option.argtypes = [vp, C.c_char_p, i64]
         L.fms_set_exchange.argtypes = [vp, EXCHANGE_FN, vp, i32, i32]
         L.fms_set_pixel_shard.argtypes = [vp, EXCHANGE_FN, vp, i32, i32, i64, i64]
+        L.fms_set_allgather.argtypes = [vp, ALLGATHER_FN, vp]
+        L.fms_nccl_unique_id.argtypes = [vp]
+        L.fms_set_nccl.argtypes = [vp, vp, i32, i32, i32, i64, i64]
+        L.fms_ctx_create_dist.argtypes = [C.POINTER(vp), C.c_int, vp, i32, i32, i32, i64, i64]
         L.fms_session_create.argtypes = [vp, C.POINTER(Policy), C.POINTER(vp)]
         L.fms_session_create.restype = C.c_int
         L.fms_session_step.argtypes = [vp, vp, i64, i32] + [f64, i32, f64, vp, vp, i32, vp, vp, C.POINTER(RunStats), vp]
@@ -97,7 +105,8 @@ def lib() -> C.CDLL:
         L.fms_cluster_batch.argtypes = [vp, vp, i32, i64, i32] + common
         L.fms_cluster_batch_host.argtypes = [vp, vp, i32, i64, i32] + common
         for fn in ("fms_default_policy", "fms_ctx_create", "fms_set_option", "fms_set_exchange",
-                   "fms_set_pixel_shard", "fms_cluster",
+                   "fms_set_pixel_shard", "fms_set_allgather", "fms_nccl_unique_id", "fms_set_nccl",
+                   "fms_ctx_create_dist", "fms_cluster",
                    "fms_cluster_batch", "fms_cluster_batch_host"):
             getattr(L, fn).restype = C.c_int
         _lib = L
@@ -162,6 +171,28 @@ class Context:
                 self._xerr = e
                 return 1
         return EXCHANGE_FN(_cb)
+
+    def set_allgather(self, fn):
+        """Seed sharding's round exchange as an all-gather (include/fms.h fms_set_allgather):
+        fn(send_ptr, recv_ptr, count, stream_ptr) gathers every rank's `count` int32 values into recv
+        (rank order), ordered on the stream; None restores the all-reduce exchange."""
+        if fn is None:
+            self._gfn = ALLGATHER_FN()
+        else:
+            def _cb(user, send, recv, count, stream, _fn=fn):
+                try:
+                    return int(_fn(send, recv, count, stream or 0))
+                except Exception as e:  # must not unwind through the C library
+                    self._xerr = e
+                    return 1
+            self._gfn = ALLGATHER_FN(_cb)
+        self._check(lib().fms_set_allgather(self.h, self._gfn, None))
+
+    def set_nccl(self, unique_id: bytes, rank: int, world: int, mode: int, n_global: int = 0, offset: int = 0):
+        """In-library NCCL sharding (include/fms.h fms_set_nccl); unique_id = the 128 bytes of
+        nccl_unique_id() from rank 0.  Collective over the `world` ranks."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        self._check(lib().fms_set_nccl(self.h, buf, int(rank), int(world), int(mode), int(n_global), int(offset)))
 
     def set_pixel_shard(self, fn, rank: int, world: int, n_global: int, offset: int):
         """Pixel sharding (include/fms.h fms_set_pixel_shard): this rank holds pixels
@@ -290,6 +321,15 @@ class Session:
             self.close()
         except Exception:
             pass
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId from the library's NCCL (include/fms.h fms_nccl_unique_id)."""
+    buf = C.create_string_buffer(128)
+    rc = lib().fms_nccl_unique_id(buf)
+    if rc != 0:
+        raise FmsError(rc, "fms_nccl_unique_id failed (libnccl.so.2 not available?)")
+    return buf.raw
 
 
 _ctxs: dict[int, Context] = {}

@@ -53,6 +53,8 @@ __device__ __forceinline__ uint32_t swz_off(int row, int chunk) {
   else return row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4);
 }
 
+constexpr int kAsgMaxList = 2048;  // frames listed per launch (larger batches walk all frames)
+
 template <int NMAX>
 __device__ __forceinline__ bool asg_frame_active(const Params& p, int f) {
   const FrameCtl& c = p.ctl[f];
@@ -64,7 +66,29 @@ __global__ void __launch_bounds__(AsgCfg<DP, NMAX>::THREADS, 1)
     assign_tc_kernel(const __grid_constant__ TMaps tm, Params p) {
   using Cfg = AsgCfg<DP, NMAX>;
   constexpr int kAsgMaxN = NMAX, kAsgGroups = Cfg::GROUPS, kAsgEpiThreads = Cfg::EPI_THREADS;
-  const long long n_items = (long long)p.B * p.n_ptiles;
+  if (NMAX > 128 && p.counters[19] <= 128) return;  // no frame of this round has 129..256 centres
+  // The CTAs split the pixel tiles of the frames this instantiation assigns (a compact list of active
+  // frames), not of all B frames: frames that finished OSOP earlier, or whose centre count belongs to
+  // the other instantiation, would otherwise leave whole CTAs idle.
+  __shared__ int s_act[kAsgMaxList];
+  __shared__ int s_sm[33];
+  const bool listed = p.B <= kAsgMaxList;
+  int n_fr = p.B;
+  if (listed) {
+    int carry = 0;
+    for (int f0 = 0; f0 < p.B; f0 += blockDim.x) {
+      const int f = f0 + threadIdx.x;
+      const int a = (f < p.B && asg_frame_active<NMAX>(p, f)) ? 1 : 0;
+      int tot;
+      const int pos = carry + block_excl_scan(a, s_sm, &tot);
+      if (a) s_act[pos] = f;
+      carry += tot;
+    }
+    __syncthreads();
+    n_fr = carry;
+  }
+  auto frame_of = [&](int fa) { return listed ? s_act[fa] : fa; };
+  const long long n_items = (long long)n_fr * p.n_ptiles;
   const int i_begin = (int)((n_items * blockIdx.x) / gridDim.x);
   const int i_end = (int)((n_items * (blockIdx.x + 1)) / gridDim.x);
   if (i_begin >= i_end) return;
@@ -104,8 +128,9 @@ __global__ void __launch_bounds__(AsgCfg<DP, NMAX>::THREADS, 1)
     int stage = 0, fcount = 0, last_f = -1, act_f = -1;
     bool act_v = false;
     uint32_t sphase = 0;
-    for (int item = i_begin, f = i_begin / p.n_ptiles, t = i_begin - f * p.n_ptiles; item < i_end;
-         ++item, t = (t + 1 == p.n_ptiles) ? (++f, 0) : t + 1) {
+    for (int item = i_begin, fa = i_begin / p.n_ptiles, t = i_begin - fa * p.n_ptiles; item < i_end;
+         ++item, t = (t + 1 == p.n_ptiles) ? (++fa, 0) : t + 1) {
+      const int f = frame_of(fa);
       if (f != act_f) { act_f = f; act_v = asg_frame_active<NMAX>(p, f); }
       if (!act_v) continue;
       if (f != last_f) {
@@ -158,8 +183,9 @@ __global__ void __launch_bounds__(AsgCfg<DP, NMAX>::THREADS, 1)
     uint32_t sphase = 0;
     uint32_t idesc = 0;
     uint64_t dch = 0, dcs = 0, dcl = 0;
-    for (int item = i_begin, f = i_begin / p.n_ptiles, t = i_begin - f * p.n_ptiles; item < i_end;
-         ++item, t = (t + 1 == p.n_ptiles) ? (++f, 0) : t + 1) {
+    for (int item = i_begin, fa = i_begin / p.n_ptiles, t = i_begin - fa * p.n_ptiles; item < i_end;
+         ++item, t = (t + 1 == p.n_ptiles) ? (++fa, 0) : t + 1) {
+      const int f = frame_of(fa);
       if (f != act_f) { act_f = f; act_v = asg_frame_active<NMAX>(p, f); }
       if (!act_v) continue;
       if (f != last_f) {
@@ -219,15 +245,16 @@ __global__ void __launch_bounds__(AsgCfg<DP, NMAX>::THREADS, 1)
     // so the active items form contiguous runs and group grp takes every kAsgGroups-th of them
     // directly (the producer and the MMA warp number the same active items 0, 1, 2, ...).
     int n_act = 0;  // active items of this CTA before the current frame
-    for (int f = i_begin / p.n_ptiles; (long long)f * p.n_ptiles < i_end; ++f) {
-      const int s0 = max(i_begin, f * p.n_ptiles), s1 = min(i_end, (f + 1) * p.n_ptiles);
+    for (int fa = i_begin / p.n_ptiles; (long long)fa * p.n_ptiles < i_end; ++fa) {
+      const int f = frame_of(fa);
+      const int s0 = max(i_begin, fa * p.n_ptiles), s1 = min(i_end, (fa + 1) * p.n_ptiles);
       if (!asg_frame_active<NMAX>(p, f)) continue;
       ++fcount;
       const int Kc = p.ctl[f].Kc;
       for (int item = s0 + (((grp - n_act) % kAsgGroups) + kAsgGroups) % kAsgGroups; item < s1;
            item += kAsgGroups) {
         const int my = n_act + (item - s0);
-        const int t = item - f * p.n_ptiles;
+        const int t = item - fa * p.n_ptiles;
         const long long px = (long long)t * kBN + q * 32 + lane;
         const uint8_t fl = px < p.n ? p.flags[flag_at(p, f, px)] : 0;  // latency overlaps the wait below
         const uint32_t db = my % kAsgGroups;

@@ -156,6 +156,7 @@ __device__ void merge_nms(const Params& p, int f, const int* vals, int P, float*
   const int Kn = s_kept;
   for (int k = threadIdx.x; k < Kn && k < p.C_cap; k += blockDim.x) p.hist[(size_t)f * p.C_cap + k] = 0;
   if (threadIdx.x == 0) {
+    atomicMax(&p.counters[19], Kn);  // the largest K of the round: which assignment kernels have work
     if (s_err) { c.status = 9; c.phase = PH_ERROR; }  // FMS_E_INTERNAL: centre capacity C_cap
     c.Kc = Kn < p.C_cap ? Kn : p.C_cap;
     c.ncand = 0;
@@ -352,6 +353,7 @@ __global__ void osop_kernel(Params p) {
   if (threadIdx.x == 0) {
     p.counters[2] = tot;
     p.counters[18] = 0;  // largest merge pool of the next round (ctl_step)
+    p.counters[19] = 0;  // largest K of the next round (merge)
   }
 }
 

@@ -318,6 +318,52 @@ __global__ void xround_unpack_kernel(Params p) {
   }
 }
 
+// all-gather layout: this rank's owned seeds j = rank + world m packed at row m; after the gather,
+// seed j of frame f sits at recv[j % world][f][j / world]
+template <int DP>
+__global__ void xgather_pack_kernel(Params p) {
+  const int f = blockIdx.y;
+  const FrameCtl& c = p.ctl[f];
+  const int K = c.phase == PH_POST ? c.K_r : 0;
+  const size_t base = (size_t)f * p.S_cap;
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < p.xkpr; m += gridDim.x * blockDim.x) {
+    const int j = p.rank + p.world * m;
+    int* row = p.xsend + ((size_t)f * p.xkpr + m) * (DP + 2);
+    const bool own = j < K;
+#pragma unroll
+    for (int k = 0; k < DP; ++k) row[k] = own ? __float_as_int(p.seeds[(base + j) * DP + k]) : 0;
+    row[DP] = own ? (int)p.sstat[base + j] : 0;
+    row[DP + 1] = own ? p.scnt[base + j] : 0;
+  }
+}
+template <int DP>
+__global__ void xgather_unpack_kernel(Params p) {
+  const int f = blockIdx.y;
+  const FrameCtl& c = p.ctl[f];
+  if (c.phase != PH_POST) return;
+  const int K = c.K_r;
+  const size_t base = (size_t)f * p.S_cap;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < K; j += gridDim.x * blockDim.x) {
+    const int* row = p.xrecv + (((size_t)(j % p.world) * p.B + f) * p.xkpr + j / p.world) * (DP + 2);
+#pragma unroll
+    for (int k = 0; k < DP; ++k) p.seeds[(base + j) * DP + k] = __int_as_float(row[k]);
+    p.sstat[base + j] = (uint8_t)row[DP];
+    p.scnt[base + j] = row[DP + 1];
+  }
+}
+cudaError_t launch_xgather(const Params& p, bool pack, cudaStream_t st) {
+  const int rows = pack ? p.xkpr : p.xkmax;
+  const dim3 g((unsigned)std::max(1, std::min(64, (rows + 255) / 256)), p.B);
+  if (p.DP == 16) {
+    if (pack) xgather_pack_kernel<16><<<g, 256, 0, st>>>(p);
+    else xgather_unpack_kernel<16><<<g, 256, 0, st>>>(p);
+  } else {
+    if (pack) xgather_pack_kernel<32><<<g, 256, 0, st>>>(p);
+    else xgather_unpack_kernel<32><<<g, 256, 0, st>>>(p);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_xchg_pack(const Params& p, cudaStream_t st) {
   xchg_pack_kernel<<<(p.B + 255) / 256, 256, 0, st>>>(p);
   return cudaGetLastError();

@@ -12,6 +12,8 @@
 //     K4 merge -> K5 assign -> K7 osop                   P:223, Eq. 19
 //   output centres
 #include <cudaTypedefs.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is opened at run time (fms_set_nccl), not linked
 
 #include <algorithm>
 #include <cmath>
@@ -49,6 +51,7 @@ cudaError_t launch_ctl(const Params& p, cudaStream_t st);
 cudaError_t launch_xchg_pack(const Params& p, cudaStream_t st);
 cudaError_t launch_xkmax(const Params& p, cudaStream_t st);
 cudaError_t launch_xround(const Params& p, bool pack, cudaStream_t st);
+cudaError_t launch_xgather(const Params& p, bool pack, cudaStream_t st);
 cudaError_t setup_assign_attrs();
 cudaError_t launch_output(const Params& p, float* centres_out, int cap, cudaStream_t st);
 cudaError_t setup_iter_attrs();
@@ -94,6 +97,9 @@ struct Ctx {
   // seed sharding: the caller's in-place int32 sum over ranks (fms_set_exchange)
   fms_exchange_fn xfn = nullptr;
   void* xuser = nullptr;
+  fms_allgather_fn gfn = nullptr;  // seed sharding: round exchange by all-gather of owned rows (optional)
+  void* guser = nullptr;
+  void* nccl_comm = nullptr;       // in-library NCCL communicator (fms_set_nccl)
   int rank = 0, world = 1;
   // pixel sharding: the caller's int32 sum; this rank holds pixels [poff, poff + n) of n_glob
   fms_exchange_fn pfn = nullptr;
@@ -252,6 +258,9 @@ size_t carve(Params& p, uint8_t* base) {
   if (p.world > 1) {  // seed-sharding exchange buffers
     p.xchg = (int*)take((size_t)B * 4 * 4);
     p.xbuf = (int*)take((size_t)B * p.S_cap * (p.DP + 2) * 4);
+    const size_t kpr = (size_t)(p.S_cap + p.world - 1) / p.world;
+    p.xsend = (int*)take((size_t)B * kpr * (p.DP + 2) * 4);
+    p.xrecv = (int*)take((size_t)p.world * B * kpr * (p.DP + 2) * 4);
   }
   return align_up(off, 1024);
 }
@@ -613,7 +622,14 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
         CU(cudaStreamSynchronize(st));
         ++syncs;
         p.xkmax = c->h_counters[8];
-        if (p.xkmax > 0) {
+        if (p.xkmax > 0 && c->gfn) {  // all-gather of every rank's owned rows (1/world of the payload each)
+          p.xkpr = (p.xkmax + p.world - 1) / p.world;
+          CU(launch_xgather(p, true, st));
+          if (c->gfn(c->guser, p.xsend, p.xrecv, (int64_t)B * p.xkpr * (p.DP + 2), st) != 0)
+            return fail(c, FMS_E_NCCL, "round all-gather failed");
+          CU(launch_xgather(p, false, st));
+          kernels += 2;
+        } else if (p.xkmax > 0) {
           CU(launch_xround(p, true, st));
           if (c->xfn(c->xuser, p.xbuf, (int64_t)B * p.xkmax * (p.DP + 2), st) != 0)
             return fail(c, FMS_E_NCCL, "round exchange failed");
@@ -723,9 +739,58 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   return result;
 }
 
+// ---- in-library NCCL (fms_set_nccl): libnccl.so.2 opened at run time, so the library loads on
+//      machines without it (a process that already loaded NCCL, e.g. through torch, shares that copy) ----
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+};
+const NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false, ok = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+      api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+      api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+      api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
+      api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+      api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+      ok = api.get_unique_id && api.comm_init_rank && api.all_reduce && api.all_gather && api.comm_destroy &&
+           api.error_string;
+    }
+  }
+  return ok ? &api : nullptr;
+}
+// the two collectives of the sharding protocols, enqueued on the library's stream
+int nccl_sum_i32(void* comm, int32_t* buf, int64_t count, void* stream) {
+  return nccl_api()->all_reduce(buf, buf, (size_t)count, ncclInt32, ncclSum, static_cast<ncclComm_t>(comm),
+                                static_cast<cudaStream_t>(stream)) == ncclSuccess ? 0 : 1;
+}
+int nccl_gather_i32(void* comm, const int32_t* send, int32_t* recv, int64_t count, void* stream) {
+  return nccl_api()->all_gather(send, recv, (size_t)count, ncclInt32, static_cast<ncclComm_t>(comm),
+                                static_cast<cudaStream_t>(stream)) == ncclSuccess ? 0 : 1;
+}
+
 }  // namespace
 
 extern "C" {
+
+fms_status fms_nccl_unique_id(void* id_out) {
+  const NcclApi* a = nccl_api();
+  if (!id_out) return FMS_E_INVALID;
+  if (!a) return FMS_E_NCCL;
+  ncclUniqueId id;
+  if (a->get_unique_id(&id) != ncclSuccess) return FMS_E_NCCL;
+  memcpy(id_out, &id, sizeof(id));
+  return FMS_OK;
+}
 
 const char* fms_version(void) { return "fms-b200 0.1 (sm_100a, tcgen05)"; }
 
@@ -771,6 +836,7 @@ void fms_ctx_destroy(void* ctx) {
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->h_prof) cudaFreeHost(c->h_prof);
   if (c->pbuf) cudaFree(c->pbuf);
+  if (c->nccl_comm && nccl_api()) nccl_api()->comm_destroy(static_cast<ncclComm_t>(c->nccl_comm));
   for (int i = 0; i < 2; ++i) {
     if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
     if (c->ev_out[i]) cudaEventDestroy(c->ev_out[i]);
@@ -810,6 +876,58 @@ fms_status fms_set_exchange(void* ctx, fms_exchange_fn fn, void* user, int32_t r
     c->prank = 0;
   }
   c->fresh_ws = true;  // the carve changes (exchange buffers)
+  return FMS_OK;
+}
+
+fms_status fms_set_nccl(void* ctx, const void* unique_id, int32_t rank, int32_t world, int32_t mode,
+                        int64_t n_global, int64_t offset) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c) return FMS_E_INVALID;
+  if (world < 1 || rank < 0 || rank >= world || (mode != FMS_SHARD_SEEDS && mode != FMS_SHARD_PIXELS) ||
+      (world > 1 && !unique_id))
+    return fail(c, FMS_E_INVALID, "need 0 <= rank < world, mode FMS_SHARD_SEEDS or FMS_SHARD_PIXELS and a unique id");
+  const NcclApi* a = nccl_api();
+  if (world > 1 && !a) return fail(c, FMS_E_NCCL, "libnccl.so.2 could not be opened");
+  if (c->nccl_comm) {
+    a->comm_destroy(static_cast<ncclComm_t>(c->nccl_comm));
+    c->nccl_comm = nullptr;
+  }
+  if (world == 1) {  // no sharding
+    fms_set_exchange(c, nullptr, nullptr, 0, 1);
+    return fms_set_pixel_shard(c, nullptr, nullptr, 0, 1, n_global, offset);
+  }
+  CU(cudaSetDevice(c->device));
+  ncclUniqueId id;
+  memcpy(&id, unique_id, sizeof(id));
+  ncclComm_t comm = nullptr;
+  const ncclResult_t r = a->comm_init_rank(&comm, world, id, rank);
+  if (r != ncclSuccess) return fail(c, FMS_E_NCCL, std::string("ncclCommInitRank: ") + a->error_string(r));
+  c->nccl_comm = comm;
+  if (mode == FMS_SHARD_SEEDS) {
+    fms_status s = fms_set_exchange(c, nccl_sum_i32, comm, rank, world);
+    if (s != FMS_OK) return s;
+    return fms_set_allgather(c, nccl_gather_i32, comm);
+  }
+  return fms_set_pixel_shard(c, nccl_sum_i32, comm, rank, world, n_global, offset);
+}
+
+fms_status fms_ctx_create_dist(void** ctx_out, int device, const void* unique_id, int32_t rank, int32_t world,
+                               int32_t mode, int64_t n_global, int64_t offset) {
+  fms_status s = fms_ctx_create(ctx_out, device);
+  if (s != FMS_OK) return s;
+  s = fms_set_nccl(*ctx_out, unique_id, rank, world, mode, n_global, offset);
+  if (s != FMS_OK) {
+    fms_ctx_destroy(*ctx_out);
+    *ctx_out = nullptr;
+  }
+  return s;
+}
+
+fms_status fms_set_allgather(void* ctx, fms_allgather_fn fn, void* user) {
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!c) return FMS_E_INVALID;
+  c->gfn = fn;
+  c->guser = user;
   return FMS_OK;
 }
 

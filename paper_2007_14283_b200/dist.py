@@ -1,5 +1,6 @@
-"""Seed sharding and pixel sharding (8(e)3) over torch.distributed: the exchange
-callback for Context.set_exchange / Context.set_pixel_shard.
+"""Seed sharding and pixel sharding (8(e)3) over torch.distributed: in-library NCCL
+(the unique id shared through torch.distributed) or the exchange / all-gather callbacks for
+Context.set_exchange / set_allgather / set_pixel_shard.
 
 The library calls the exchange at its two collective points (per lockstep step: per-frame counts;
 per round: the owners' converged seeds) with an int32 device buffer and its stream; this module
@@ -40,15 +41,56 @@ def make_exchange(group=None):
     return exchange
 
 
-def enable_seed_sharding(ctx, group=None):
+def make_allgather(group=None):
+    """The all-gather of seed sharding's round exchange: rank r's `count` int32 values land at
+    recv[r * count, (r + 1) * count)."""
+    backend = dist.get_backend(group)
+    world = dist.get_world_size(group)
+
+    def allgather(send_ptr: int, recv_ptr: int, count: int, stream: int) -> int:
+        s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            snd = torch.as_tensor(_DevBuf(send_ptr, count), device="cuda")
+            rcv = torch.as_tensor(_DevBuf(recv_ptr, count * world), device="cuda")
+            if backend == "nccl":
+                dist.all_gather_into_tensor(rcv, snd, group=group)
+            else:
+                h = snd.cpu()  # synchronous on s
+                parts = [torch.empty_like(h) for _ in range(world)]
+                dist.all_gather(parts, h, group=group)
+                rcv.copy_(torch.cat(parts))
+                s.synchronize()
+        return 0
+
+    return allgather
+
+
+def _share_unique_id(group=None) -> bytes:
+    import paper_2007_14283_b200 as fms
+    obj = [fms.nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
+def enable_seed_sharding(ctx, group=None, in_library=None):
     """Make `ctx` iterate only this rank's share of every round's seeds (all ranks must call the
-    clustering entry points with identical inputs; each returns the full result)."""
+    clustering entry points with identical inputs; each returns the full result).  With the NCCL
+    backend the collectives run as NCCL calls inside the library (include/fms.h fms_set_nccl: no
+    Python callback per lockstep step); otherwise (gloo: tests with several ranks on one GPU) through
+    the callbacks above, the round exchange as an all-gather of owned rows."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     if world == 1:
         ctx.set_exchange(None, 0, 1)
+        return ctx
+    if in_library is None:
+        in_library = dist.get_backend(group) == "nccl"
+    if in_library:
+        import paper_2007_14283_b200 as fms
+        ctx.set_nccl(_share_unique_id(group), rank, world, fms.SHARD_SEEDS)
     else:
         ctx.set_exchange(make_exchange(group), rank, world)
+        ctx.set_allgather(make_allgather(group))
     return ctx
 
 
@@ -62,7 +104,7 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     return lo, lo + q + (1 if rank < r else 0)
 
 
-def enable_pixel_sharding(ctx, n_global: int, group=None):
+def enable_pixel_sharding(ctx, n_global: int, group=None, in_library=None):
     """Make `ctx` cluster frames of n_global pixels of which this rank holds shard_range(n_global, rank,
     world): pass this rank's rows to the clustering calls; every rank returns the same centres and K,
     and labels for its own rows.  Returns (lo, hi)."""
@@ -72,5 +114,11 @@ def enable_pixel_sharding(ctx, n_global: int, group=None):
         ctx.set_pixel_shard(None, 0, 1, n_global, 0)
         return 0, n_global
     lo, hi = shard_range(n_global, rank, world)
-    ctx.set_pixel_shard(make_exchange(group), rank, world, n_global, lo)
+    if in_library is None:
+        in_library = dist.get_backend(group) == "nccl"
+    if in_library:
+        import paper_2007_14283_b200 as fms
+        ctx.set_nccl(_share_unique_id(group), rank, world, fms.SHARD_PIXELS, n_global, lo)
+    else:
+        ctx.set_pixel_shard(make_exchange(group), rank, world, n_global, lo)
     return lo, hi

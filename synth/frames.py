@@ -197,3 +197,65 @@ def make_stack(T: int, seed: int, H: int = 512, W: int = 512, D: int = 16, cells
             g /= np.sqrt(np.sum(g * g))
             dirs[k] = np.cos(turn_rad) * dirs[k] + np.sin(turn_rad) * g
     return emb, truth
+
+
+# ------------------------------------------------------------------------------------------------
+# The paper's simulation suite (NEXT-3): the section 4.2.1 data sets of Fig. 4 and the Appendix A
+# overlap frames.  Data generation only.
+# ------------------------------------------------------------------------------------------------
+
+def make_circles(seed: int, n: int = 1500, k: int = 10, noise: float = 0.02):
+    """PAPER.md P:331 (Fig. 4, row 1): n = 1,500 2-D points evenly in k = 10 clusters on two
+    concentric circles; a cluster is an angular position, alternate clusters on the large (radius
+    U[0.95, 1.05]) and small (U[0.475, 0.525]) circle ("variations ... 10% of the circles' radius");
+    Gaussian noise of standard deviation 0.02 on both coordinates.  Returns (emb float32 [n, 2],
+    truth int32 [n]) in random order."""
+    rng = np.random.default_rng(np.random.SeedSequence([int(seed), 4201]))
+    truth = rng.permutation(np.arange(n) % k).astype(np.int32)
+    theta = 2.0 * np.pi * truth / k + 0.3
+    big = truth % 2 == 0
+    rad = np.where(big, rng.uniform(0.95, 1.05, n), rng.uniform(0.475, 0.525, n))
+    x = np.stack([rad * np.cos(theta), rad * np.sin(theta)], axis=1) + noise * rng.standard_normal((n, 2))
+    return np.ascontiguousarray(x, dtype=np.float32), truth
+
+
+def make_polarized(seed: int, instances: int, n: int = 1500, background: int = 750, noise: float | None = None):
+    """PAPER.md P:331 (Fig. 4, rows 2-3): polarized 2-D data with a background cluster of 750 of the
+    1,500 points ("accounting for 50% of the total points") and `instances` = 7 or 3 further
+    clusters sharing the rest evenly; radii ("intensity") U[1, 2]; Gaussian noise of standard deviation
+    0.005 (seven instances) or 0.01 (three instances).  The k = instances + 1 cluster directions are
+    evenly spaced angles.  Returns (emb float32 [n, 2], truth int32 [n]; 0 = background)."""
+    rng = np.random.default_rng(np.random.SeedSequence([int(seed), 4202, instances]))
+    if noise is None:
+        noise = 0.005 if instances == 7 else 0.01
+    k = instances + 1
+    sizes = [background] + [(n - background) // instances + (1 if j < (n - background) % instances else 0)
+                            for j in range(instances)]
+    truth = rng.permutation(np.repeat(np.arange(k), sizes)).astype(np.int32)
+    theta = 2.0 * np.pi * truth / k + 0.2
+    rad = rng.uniform(1.0, 2.0, n)
+    x = np.stack([rad * np.cos(theta), rad * np.sin(theta)], axis=1) + noise * rng.standard_normal((n, 2))
+    return np.ascontiguousarray(x, dtype=np.float32), truth
+
+
+def make_overlap(spacing: float, H: int = 1000, W: int = 1000, D: int = 18, circles: int = 8, diameter: int = 250):
+    """PAPER.md P:533-541 (Appendix A): a 1000 x 1000 x 18 frame with eight foreground circles of
+    diameter 250 px, each with its own cosine embedding (signed basis directions, orthogonal to the
+    background's), no noise; the overlap level is set by the distance `spacing` (px) between
+    neighbouring circle centres, placed on a ring around the frame centre (spacing >= 250: no
+    overlap).  Later circles are drawn over earlier ones.  Returns (emb float32 [H W, D], truth int32
+    [H W]; 0 = background, k = circle k)."""
+    R = diameter / 2.0
+    ring = spacing / (2.0 * np.sin(np.pi / circles))  # chord between neighbours = spacing
+    cy0, cx0 = H / 2.0, W / 2.0
+    dirs = np.zeros((circles + 1, D))
+    for k in range(circles + 1):
+        dirs[k, k // 2] = 1.0 if k % 2 == 0 else -1.0
+    yy, xx = np.mgrid[0:H, 0:W]
+    truth = np.zeros((H, W), dtype=np.int32)
+    for k in range(circles):
+        a = 2.0 * np.pi * k / circles
+        cy, cx = cy0 + ring * np.sin(a), cx0 + ring * np.cos(a)
+        truth[(yy + 0.5 - cy) ** 2 + (xx + 0.5 - cx) ** 2 <= R * R] = k + 1
+    truth = truth.reshape(-1)
+    return np.ascontiguousarray(dirs[truth], dtype=np.float32), truth
