@@ -65,10 +65,13 @@ struct Iter8Cfg {
   // integers) instead of shared-memory segment sums, which leaves room for a deeper pixel ring
   static constexpr bool DIRECT = DP == 32;
   static constexpr int GROUP_WARPS = k8::kEpiWarps / GROUPS;  // a multiple of 4 (one per lane quarter)
-  // (2 groups of 8 warps hung in a probe run at DP = 16 and is not used; 4 is the tested layout)
+  // 4 groups of 4 warps is the tested layout.  2 groups of 8 and 1 group of 16 (every warp on every
+  // tile, 32 columns each: 16 TMEM loads in flight per tile) hung in probe runs -- a timing-dependent
+  // race not found yet (a debug build with slower waits completes) -- and are not used.
   static_assert(GROUPS == 4, "epilogue layout: 4 groups of 4 warps");
   static constexpr int COLS_PER_WARP = kBN / (GROUP_WARPS / 4);
-  static constexpr int PARTS = COLS_PER_WARP / 64;            // 64-column tcgen05.ld per part
+  static constexpr int PART = COLS_PER_WARP < 64 ? COLS_PER_WARP : 64;  // columns per tcgen05.ld
+  static constexpr int PARTS = COLS_PER_WARP / PART;
   static constexpr int ROW_B = DP * 2;                    // bytes per fp16 row
   static constexpr int TILE_B = kBN * ROW_B;              // one pixel tile (one limb)
   static constexpr int A_B = kBM * ROW_B;                 // one seed tile (one split)
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
   using namespace k8;
   using Cfg = Iter8Cfg<DP>;
   constexpr int kGroups = Cfg::GROUPS, kGroupWarps = Cfg::GROUP_WARPS;
-  constexpr int kColsPerWarp = Cfg::COLS_PER_WARP, kParts = Cfg::PARTS;
+  constexpr int kColsPerWarp = Cfg::COLS_PER_WARP, kParts = Cfg::PARTS, kPart = Cfg::PART;
   const int n_items = p.counters[0];
   const int ct = p.counters[12];   // pixel tiles per work item
   const int nch = p.counters[13];  // work items per seed tile
@@ -422,14 +425,14 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
         bool p_free = !need_free;
 #pragma unroll
         for (int part = 0; part < kParts; ++part) {
-          const uint32_t col = (uint32_t)(h * kColsPerWarp + part * 64);
-          uint32_t v[64];
+          const uint32_t col = (uint32_t)(h * kColsPerWarp + part * kPart);
+          uint32_t v[kPart];
           if (!K8_SKIP(4)) {
-            tmem_ld64(tmem + lane_base + cb * kBN + col, v);
+            tmem_ld_n<kPart>(tmem + lane_base + cb * kBN + col, v);
             tmem_ld_wait();
           } else {
 #pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] = __float_as_uint(tau_m) + (uint32_t)(i * lane);
+            for (int i = 0; i < kPart; ++i) v[i] = __float_as_uint(tau_m) + (uint32_t)(i * lane);
           }
           if (part == kParts - 1) {
             K8_TL(role, ctile, 2);
@@ -438,10 +441,10 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
             if (lane == 0) mbar_arrive(&c_empty[cb]);  // MMA1 may overwrite C[cb]
           }
           if (!p_free) p_free = mbar_test(&q_empty[u % Cfg::QSTAGES], (u / Cfg::QSTAGES) & 1);
-          uint32_t pk[16];
+          uint32_t pk[kPart / 4];
           if (!K8_SKIP(8)) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
+            for (int i = 0; i < kPart / 4; ++i) {
               uint32_t d0, d1, d2, d3;
               sub_tau2(v[4 * i], v[4 * i + 1], tau_m, d0, d1);
               sub_tau2(v[4 * i + 2], v[4 * i + 3], tau_m, d2, d3);
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) pk[i] = v[4 * i] ^ v[4 * i + 3];
+            for (int i = 0; i < kPart / 4; ++i) pk[i] = v[4 * i] ^ v[4 * i + 3];
           }
           K8_TL(role, ctile, 3);
           if (!p_free) {
@@ -460,14 +463,14 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
           if (w.mode == 0) {
             tc_fence_after();
             if (!K8_SKIP(16)) {
-              tmem_st16(tmem + lane_base + Cfg::P_COL + pb * (kBN / 4) + col / 4, pk);
+              tmem_st_n<kPart / 4>(tmem + lane_base + Cfg::P_COL + pb * (kBN / 4) + col / 4, pk);
             } else {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) cnt += pk[i] & 1u;  // keeps the ALU work alive
+              for (int i = 0; i < kPart / 4; ++i) cnt += pk[i] & 1u;  // keeps the ALU work alive
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) cnt += __popc(pk[i]);  // 8 bits per member
+            for (int i = 0; i < kPart / 4; ++i) cnt += __popc(pk[i]);  // 8 bits per member
           }
         }
         if (w.mode == 0 && !K8_SKIP(16)) tmem_st_wait();
