@@ -65,10 +65,11 @@ struct Iter8Cfg {
   // integers) instead of shared-memory segment sums, which leaves room for a deeper pixel ring
   static constexpr bool DIRECT = DP == 32;
   static constexpr int GROUP_WARPS = k8::kEpiWarps / GROUPS;  // a multiple of 4 (one per lane quarter)
-  // 4 groups of 4 warps is the tested layout.  2 groups of 8 and 1 group of 16 (every warp on every
-  // tile, 32 columns each: 16 TMEM loads in flight per tile) hung in probe runs -- a timing-dependent
-  // race not found yet (a debug build with slower waits completes) -- and are not used.
-  static_assert(GROUPS == 4, "epilogue layout: 4 groups of 4 warps");
+  // 4 groups of 4 warps (the default) or 1 group of 16 warps (every warp on every tile, 32 columns
+  // each: 16 TMEM loads in flight per tile; measured slower, 906 vs 805 cycles per tile).  2 groups
+  // of 8 are excluded: with NC = 3 the MMA1 issuer can complete a group's c_full twice before a slow
+  // warp of the group waits on it (parity aliasing), which deadlocked in a probe run.
+  static_assert(GROUPS == 4 || GROUPS == 1, "epilogue layout: 4 groups of 4 warps, or 1 group of 16");
   static constexpr int COLS_PER_WARP = kBN / (GROUP_WARPS / 4);
   static constexpr int PART = COLS_PER_WARP < 64 ? COLS_PER_WARP : 64;  // columns per tcgen05.ld
   static constexpr int PARTS = COLS_PER_WARP / PART;
@@ -189,8 +190,12 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
   // similarity ready: one barrier per epilogue GROUP (not per C buffer), so that a group never waits
   // on a barrier whose previous phase is still pending (a waiter two phases ahead would see the
   // pending phase's parity as complete)
-  uint64_t* c_full = a_empty + 2;             // [kGroups]
-  uint64_t* c_empty = c_full + kGroups;       // [NC] similarity loaded by the epilogue
+  // c_full: per group with 4 groups (safe because MMA1 issues in order and NC < 4: the group's next
+  // phase needs the group's previous tile consumed), per C buffer with 1 group (every warp consumes
+  // every tile, so a buffer's next phase needs every waiter's release)
+  constexpr int kCF = kGroups == 1 ? Cfg::NC : kGroups;
+  uint64_t* c_full = a_empty + 2;             // [kCF]
+  uint64_t* c_empty = c_full + kCF;           // [NC] similarity loaded by the epilogue
   // an item's Gq complete: per group -- the group owning the item's last tile drains it, and each
   // group's drains are sequential in its own program order
   uint64_t* g_full = c_empty + Cfg::NC;       // [kGroups]
@@ -209,7 +214,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
     for (int i = 0; i < 2; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < kGroups; ++i) mbar_init(&g_full[i], 1);
     mbar_init(g_empty, 4);  // drained by 4 warps (one per lane quarter)
-    for (int i = 0; i < kGroups; ++i) mbar_init(&c_full[i], 1);
+    for (int i = 0; i < kCF; ++i) mbar_init(&c_full[i], 1);
     for (int i = 0; i < Cfg::NC; ++i) mbar_init(&c_empty[i], kGroupWarps);
     for (int i = 0; i < Cfg::NP; ++i) mbar_init(&p_full[i], kGroupWarps);
     fence_barrier_init();
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
           for (int kk = 0; kk < DP / 16; ++kk)  // + s_lo . hi
             mma_ss_f16_el(d, dal + kk * 2, dxh + kk * 2, IDESC1, 1u);
         }
-        tc_commit_el(&c_full[i % kGroups]);
+        tc_commit_el(&c_full[kGroups == 1 ? buf : i % kGroups]);
         tc_commit_el(&x_empty[stage]);  // the limbs stage is free once these MMAs complete
         K8_TL(1, i, 3);
         if (++stage == Cfg::LSTAGES) { stage = 0; sphase ^= 1; }
@@ -414,7 +419,8 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
         const int role = 3 + (grp * kGroupWarps + (warp % kGroupWarps)) % 16;
         (void)role;
         K8_TL(role, ctile, 0);
-        mbar_wait(&c_full[grp], mine & 1);
+        if (kGroups == 1) mbar_wait(&c_full[cb], (ctile / Cfg::NC) & 1);
+        else mbar_wait(&c_full[grp], mine & 1);
         ++mine;
         K8_TL(role, ctile, 1);
         tc_fence_after();
