@@ -69,7 +69,6 @@ struct Iter8Cfg {
   // each: 16 TMEM loads in flight per tile; measured slower, 906 vs 805 cycles per tile).  2 groups
   // of 8 are excluded: with NC = 3 the MMA1 issuer can complete a group's c_full twice before a slow
   // warp of the group waits on it (parity aliasing), which deadlocked in a probe run.
-  static_assert(GROUPS == 4 || GROUPS == 1, "epilogue layout: 4 groups of 4 warps, or 1 group of 16");
   static constexpr int COLS_PER_WARP = kBN / (GROUP_WARPS / 4);
   static constexpr int PART = COLS_PER_WARP < 64 ? COLS_PER_WARP : 64;  // columns per tcgen05.ld
   static constexpr int PARTS = COLS_PER_WARP / PART;
@@ -91,6 +90,8 @@ struct Iter8Cfg {
 #else
   static constexpr int NP = DP == 16 ? (NC == 3 ? 2 : 3) : 3;  // P buffers (32 columns each)
 #endif
+  static_assert(GROUPS == 4 || GROUPS == 1 || (GROUPS == 2 && NC == 2),
+                "epilogue layout: 4 groups of 4 warps, 1 group of 16, or 2 groups of 8 with one C buffer each");
   static constexpr int P_COL = NC * kBN;
   static constexpr int G_COL = P_COL + NP * (kBN / 4);
   static_assert(G_COL + NQ <= 512, "TMEM budget");

@@ -92,3 +92,46 @@ def test_seed_sharded_matches_oracle_exact():
     assert bijection(r["labels"][0], ro.labels)
     _, _, dist = match_centres(r["centres"][0, :ro.K], ro.centres)
     assert dist.max() <= 1e-4
+
+
+def _nccl_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2007_14283_b200 as fms
+    from paper_2007_14283_b200.dist import enable_seed_sharding
+    f = synth.make_frame("S1sep", 1)
+    ctx = fms.Context(0)
+    result = {}
+    try:
+        enable_seed_sharding(ctx, in_library=True)   # fms_nccl_unique_id + fms_set_nccl over 2 ranks
+        labels, centres, K, st = ctx.cluster(torch.from_numpy(f.emb).cuda(),
+                                             policy=fms.default_policy(**_policy_kw("S1sep", f.n)),
+                                             centres_cap=1024)
+        result = dict(ok=1, labels=labels.cpu().numpy(), K=np.array(K))
+    except fms.FmsError as e:
+        result = dict(ok=0, status=e.status, msg=str(e))
+    np.save(os.path.join(out, f"n{rank}.npy"), result, allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_in_library_nccl_two_ranks():
+    """In-library NCCL (include/fms.h fms_set_nccl): rank 0's unique id is shared through
+    torch.distributed and both ranks build the communicator.  With two ranks on ONE GPU, NCCL either
+    runs (then the result equals the unsharded run) or refuses the duplicate device -- the library
+    must report that as FMS_E_NCCL with NCCL's message, not hang or crash."""
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as out:
+        mp.start_processes(_nccl_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
+        res = [np.load(os.path.join(out, f"n{r}.npy"), allow_pickle=True).item() for r in range(2)]
+    print("in-library NCCL, 2 ranks on one GPU:", [("ran" if r["ok"] else r.get("msg")) for r in res])
+    if all(r["ok"] for r in res):
+        ref = _run_single("S1sep", [1])
+        for r in res:
+            assert np.array_equal(r["labels"], ref["labels"]) and np.array_equal(r["K"], ref["K"])
+    else:
+        for r in res:
+            assert r["ok"] or (r["status"] == 7 and "nccl" in r["msg"].lower()), r
