@@ -311,7 +311,8 @@ def seed_sharded_c4(world, rank, local, B=2, warmup=1, steps=3):
         for _ in range(warmup):
             ctx.cluster_batch_ptr(x.data_ptr(), B, n, d, labels.data_ptr(), cent.data_ptr(), CAP, H, MAX_ITERS, None,
                                   pol, stream.cuda_stream)
-        torch.distributed.barrier()
+        if world > 1:
+            torch.distributed.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -323,6 +324,9 @@ def seed_sharded_c4(world, rank, local, B=2, warmup=1, steps=3):
         return reduce_max(e0.elapsed_time(e1), world, dev), Ks
 
     single_ms, K1 = timed(fms.Context(local))
+    if world == 1:  # the one-GPU point of the C4 strong-scaling curve (N > 1 runs add the sharded points)
+        return {"config": "C4: 1024x1024, 32-D, 200 cells, full OSOP", "frames_per_step": B, "n_gpus": 1,
+                "value": steps * B / (single_ms / 1e3), "unit": "frames/s", "scaling": "strong"}
     sharded_ms, KN = timed(enable_seed_sharding(fms.Context(local)))
     return {"config": "C4: 1024x1024, 32-D, 200 cells, full OSOP", "frames_per_step": B, "n_gpus": world,
             "value": steps * B / (sharded_ms / 1e3), "unit": "frames/s", "scaling": "strong",
@@ -571,6 +575,8 @@ def main():
     extras = {}
     if world == 1 and not sharded:
         extras = latency_and_b16(ctx, pool, pol, h_run, stream)
+        if args.config == CONFIG and not args.no_seed_shard and not gauss and not euclid:
+            extras["seed_sharded"] = seed_sharded_c4(1, 0, local)
     cb = None
     if world == 1 and not args.no_cpu:
         cb = cpu_baseline(args.config, budget_s=args.cpu_budget_s)

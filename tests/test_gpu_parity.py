@@ -379,3 +379,16 @@ def test_internal_capacity_is_not_capacity_status():
     lg, cg, Kg, st = run_gpu(f.emb, cap=3, allow=(5,), n_seeds=64, min_instance_px=min_instance_px(f.n))
     assert st["status"] == 5 and Kg[0] == f.cells + 1
     assert np.all((lg[0] >= 0) & (lg[0] < Kg[0]))
+
+
+def test_c4_paper_defaults_no_capacity_error():
+    """VERDICT r01 missing #8 'done' criterion: a C4 frame (1024x1024, 32-D, ~200 cells) at the paper's
+    defaults (no size floor, no saturation stop: the controller seeds up to L N_min, thousands of
+    seeds) clusters without a capacity error -- pools above 8192 take the global-memory merge."""
+    f = synth.make_frame("C4", 1)
+    lg, cg, Kg, st = run_gpu(f.emb, cap=8192, rng_seed=0)
+    fr = st["frames"][0]
+    assert st["status"] == 0 and fr["status"] == 0
+    assert 0 < Kg[0] <= 8192 and lg[0].min() >= 0 and lg[0].max() < Kg[0]
+    assert fr["seeds_total"] > 2048 and fr["rounds"] >= 3
+    assert np.abs(np.linalg.norm(cg[0, :Kg[0]], axis=1) - 1.0).max() <= 1e-5
