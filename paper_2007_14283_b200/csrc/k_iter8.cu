@@ -114,6 +114,7 @@ struct Iter8Cfg {
 // [nch tile_off(f), nch (tile_off(f) + T_f)), so the tile task at item / nch belongs to f.
 struct Item8 {
   int f, tile, chunk, mode, key;  // key: frame * S_pad + tile * kBM (the segment a G drain belongs to)
+  int rows;                       // active seed rows in the tile (the last tile of a frame is partial)
 };
 __device__ __forceinline__ Item8 item8(const Params& p, int item, int nch) {
   const int f = p.tiles[item / nch].f;
@@ -122,7 +123,7 @@ __device__ __forceinline__ Item8 item8(const Params& p, int item, int nch) {
   const int L = item - nch * c.tile_off;
   const int chunk = L / T;
   const TileTask tt = p.tiles[c.tile_off + (L - chunk * T)];
-  return Item8{f, tt.tile, chunk, tt.mode, f * p.S_pad + tt.tile * kBM};
+  return Item8{f, tt.tile, chunk, tt.mode, f * p.S_pad + tt.tile * kBM, min(kBM, c.n_active - tt.tile * kBM)};
 }
 
 // two in-window differences per instruction: {c0 - tau_m, c1 - tau_m}
@@ -430,8 +431,17 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
         const uint32_t u = ctile - Cfg::NP;
         const bool need_free = ctile >= (uint32_t)Cfg::NP;
         bool p_free = !need_free;
+        // a lane quarter without active seeds (the tail of a frame's last seed tile) skips its C loads,
+        // flat kernel and weight stores; its rows of Gq are never drained (stale weights only reach them)
+        const bool quarter_active = q * 32 < w.rows;
+        if (!quarter_active) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&c_empty[cb]);
+          if (!p_free) mbar_wait(&q_empty[u % Cfg::QSTAGES], (u / Cfg::QSTAGES) & 1);
+        }
 #pragma unroll
-        for (int part = 0; part < kParts; ++part) {
+        for (int part = 0; part < kParts && quarter_active; ++part) {
           const uint32_t col = (uint32_t)(h * kColsPerWarp + part * kPart);
           uint32_t v[kPart];
           if (!K8_SKIP(4)) {
@@ -491,7 +501,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
           ++drains;
           K8_TL(role, ctile, 6);
           tc_fence_after();
-          if (w.mode == 0) {
+          if (w.mode == 0 && quarter_active) {
             if (!Cfg::DIRECT && seg != w.key) {
               flush();
               seg = w.key;

@@ -3,7 +3,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Ipaper_2007_14283_b200/csrc \
 //        -Iinclude -o tools/iter8_probe tools/iter8_probe.cu paper_2007_14283_b200/csrc/k_iter8.cu \
 //        paper_2007_14283_b200/csrc/k_iter.cu -lcuda
-// Run:   tools/iter8_probe [B=32] [T=2] [ct=64] [n=262144] [DP=16]
+// Run:   tools/iter8_probe [B=32] [T=2] [ct=64] [n=262144] [DP=16] [rows per frame = 128 T]
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -67,6 +67,8 @@ int main(int argc, char** argv) {
   const int ct = argc > 3 ? atoi(argv[3]) : 64;
   const long long n = argc > 4 ? atoll(argv[4]) : 262144;
   const int DP = argc > 5 ? atoi(argv[5]) : 16;
+  // active seed rows per frame (default: every tile full); the last tile of a frame is partial otherwise
+  const int rows = argc > 6 ? atoi(argv[6]) : T_per_frame * 128;
   const long long n_pad = (n + 127) / 128 * 128;
   const int S_pad = 128 * T_per_frame;
   setup_iter_attrs();
@@ -111,7 +113,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&p.tiles, T * sizeof(TileTask));
   cudaMemcpy(p.tiles, tt.data(), T * sizeof(TileTask), cudaMemcpyHostToDevice);
   std::vector<FrameCtl> hc(B);
-  for (int f = 0; f < B; ++f) { memset(&hc[f], 0, sizeof(FrameCtl)); hc[f].tile_off = f * T_per_frame; hc[f].n_tiles_step = T_per_frame; }
+  for (int f = 0; f < B; ++f) { memset(&hc[f], 0, sizeof(FrameCtl)); hc[f].tile_off = f * T_per_frame; hc[f].n_tiles_step = T_per_frame; hc[f].n_active = rows; }
   cudaMalloc(&p.ctl, B * sizeof(FrameCtl));
   cudaMemcpy(p.ctl, hc.data(), B * sizeof(FrameCtl), cudaMemcpyHostToDevice);
   cudaMalloc(&p.counters, 64 * 4);
