@@ -27,6 +27,11 @@ src = subprocess.check_output(["ncu", "-i", rep, "--page", "source", "--csv", "-
 rows = list(csv.reader(io.StringIO(src)))
 hdr = rows[1]
 R = rows[2:]
+# a capture of several launches repeats the header per launch: keep the first launch's rows
+for k, r in enumerate(R):
+    if "Address" in r or "Kernel Name" in r:
+        R = R[:k]
+        break
 ix = {h: i for i, h in enumerate(hdr)}
 base = int(R[0][ix["Address"]], 16)
 S = "Warp Stall Sampling (All Samples)"
@@ -41,6 +46,9 @@ for r in R:
 T = sum(tot.values())
 E = sum(ex.values())
 print(f"samples {T}  warp instructions {E}")
-for ln, v in sorted(tot.items(), key=lambda x: -x[1])[:top]:
+import os
+key = ex if os.environ.get("SORT") == "exec" else tot
+for ln, v in sorted(key.items(), key=lambda x: -x[1])[:top]:
+    v = tot[ln]
     st = dict(sorted(((k.replace("stall_", ""), c) for k, c in agg[ln].items() if c), key=lambda x: -x[1])[:4])
     print(f"{ln[0]}:{ln[1]:<5} {v:6d} {100 * v / T:5.1f}%  exec {ex[ln]:9d} {st}")
