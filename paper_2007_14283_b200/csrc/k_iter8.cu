@@ -34,9 +34,9 @@
 //                                (hi, lo limbs; digit planes).
 //   * warp 17  : MMA1 issuer  -- C[i % NC] = 3 MMAs (M=128, N=128, K=DP) into TMEM.
 //   * warp 18  : MMA2 issuer  -- Gq += P[i % NP] . Q (kind::i8, A = P from TMEM, N = 3 DP).
-//   * warps 0-15: epilogue    -- two groups of 8 warps take alternate tiles: one tcgen05.ld of 64
-//                                columns of C per warp, C handed back to MMA1, flat kernel -> u8
-//                                weights (tcgen05.st of 16 columns).  The group that handled an
+//   * warps 0-15: epilogue    -- four groups of 4 warps take tiles round-robin: two tcgen05.ld of 64
+//                                columns of C per warp, C handed back to MMA1 (named barrier), flat
+//                                kernel -> u8 weights (tcgen05.st).  The group that handled an
 //                                item's last tile drains Gq into its own int64 segment sums.
 //                                Count-pass items (mode 1: the converged modes of a round) skip the
 //                                weighted sum and count window members (intensity, R10).
@@ -46,7 +46,11 @@
 namespace fms {
 
 namespace k8 {
+#ifdef K8_EPI_WARPS
+constexpr int kEpiWarps = K8_EPI_WARPS;
+#else
 constexpr int kEpiWarps = 16;
+#endif
 constexpr int kWarpTma = kEpiWarps, kWarpMma1 = kEpiWarps + 1, kWarpMma2 = kEpiWarps + 2;
 constexpr int kWarpTmaQ = kEpiWarps + 3;  // producer of the digit-plane ring
 constexpr int kThreads = (kEpiWarps + 4) * 32;
@@ -57,7 +61,7 @@ struct Iter8Cfg {
   // epilogue groups (tiles in flight): 4 groups of 4 warps for 16-lane rows; 32-lane rows keep 2
   // groups of 8 (their segment sums and pixel stages would not fit shared memory with 4)
 #ifdef K8_GROUPS
-  static constexpr int GROUPS = K8_GROUPS;
+  static constexpr int GROUPS = (DP == 16 || k8::kEpiWarps != 16) ? K8_GROUPS : 4;
 #else
   static constexpr int GROUPS = 4;
 #endif
@@ -70,7 +74,12 @@ struct Iter8Cfg {
   // of 8 are excluded: with NC = 3 the MMA1 issuer can complete a group's c_full twice before a slow
   // warp of the group waits on it (parity aliasing), which deadlocked in a probe run.
   static constexpr int COLS_PER_WARP = kBN / (GROUP_WARPS / 4);
-  static constexpr int PART = COLS_PER_WARP < 64 ? COLS_PER_WARP : 64;  // columns per tcgen05.ld
+#ifdef K8_PART
+  static constexpr int PART_MAX = K8_PART;
+#else
+  static constexpr int PART_MAX = 64;
+#endif
+  static constexpr int PART = COLS_PER_WARP < PART_MAX ? COLS_PER_WARP : PART_MAX;  // columns per tcgen05.ld
   static constexpr int PARTS = COLS_PER_WARP / PART;
   static constexpr int ROW_B = DP * 2;                    // bytes per fp16 row
   static constexpr int TILE_B = kBN * ROW_B;              // one pixel tile (one limb)
@@ -81,7 +90,7 @@ struct Iter8Cfg {
   static constexpr int Q_B = NQ * kBN;                    // digit planes of one tile (128 B rows, SW128)
   static constexpr int L_B = 2 * TILE_B;                  // one stage of the limb ring (hi, lo)
 #ifdef K8_NC
-  static constexpr int NC = K8_NC;
+  static constexpr int NC = DP == 16 ? K8_NC : 2;
 #else
   static constexpr int NC = DP == 16 ? 3 : 2;             // C buffers
 #endif
@@ -90,7 +99,7 @@ struct Iter8Cfg {
 #else
   static constexpr int NP = DP == 16 ? (NC == 3 ? 2 : 3) : 3;  // P buffers (32 columns each)
 #endif
-  static_assert(GROUPS == 4 || GROUPS == 1 || (GROUPS == 2 && NC == 2),
+  static_assert(GROUPS >= 1 && GROUPS <= 4 && k8::kEpiWarps % (4 * GROUPS) == 0,
                 "epilogue layout: 4 groups of 4 warps, 1 group of 16, or 2 groups of 8 with one C buffer each");
   static constexpr int P_COL = NC * kBN;
   static constexpr int G_COL = P_COL + NP * (kBN / 4);
@@ -163,6 +172,14 @@ __device__ __forceinline__ uint32_t pack_w4(uint32_t d0, uint32_t d1, uint32_t d
   } while (0)
 #endif
 
+// Epilogue -> issuer hand-offs are named barriers (bar.arrive by the group's warps, bar.sync by the MMA
+// warp; ~30 cycles against ~180 for an mbarrier arrive -> wait, tools/sync_probe.cu): one per C buffer
+// (ids 1..NC) and one per weight buffer (ids NC + 1..NC + NP).  No arrival can run a phase ahead: a
+// group's next arrival on a buffer's barrier needs an MMA that the waiting warp issues only after its
+// sync (C: the buffer's next similarity; P: the weighted sum that frees the buffer).
+// (r2: 798 -> 762 cycles per tile at 2 seed tiles per frame, 790 -> 709 at 1; tools/k9_variants.sh)
+#define K8_RELEASE_C(cb) nbar_arrive(1 + (int)(cb), (kGroupWarps + 1) * 32)
+
 template <int DP>
 __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_constant__ TMaps tm, Params p) {
   using namespace k8;
@@ -195,16 +212,17 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
   // c_full: per group with 4 groups (safe because MMA1 issues in order and NC < 4: the group's next
   // phase needs the group's previous tile consumed), per C buffer with 1 group (every warp consumes
   // every tile, so a buffer's next phase needs every waiter's release)
-  constexpr int kCF = kGroups == 1 ? Cfg::NC : kGroups;
+  // (2 groups: per C buffer as well -- a buffer's next phase needs its previous tile's group to have
+  // released it, hence to have waited)
+  constexpr int kCF = kGroups != 4 ? Cfg::NC : kGroups;
   uint64_t* c_full = a_empty + 2;             // [kCF]
-  uint64_t* c_empty = c_full + kCF;           // [NC] similarity loaded by the epilogue
   // an item's Gq complete: per group -- the group owning the item's last tile drains it, and each
   // group's drains are sequential in its own program order
-  uint64_t* g_full = c_empty + Cfg::NC;       // [kGroups]
+  uint64_t* g_full = c_full + kCF;           // [kGroups]
   uint64_t* g_empty = g_full + kGroups;       // [1] Gq drained
-  uint64_t* p_full = g_empty + 1;             // [NP] weights written
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(p_full + Cfg::NP);
-  static_assert((Cfg::LSTAGES * 2 + Cfg::QSTAGES * 2 + 5 + 2 * kGroups + Cfg::NC + Cfg::NP) * 8 + 4 <= 1024,
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(g_empty + 1);
+  static_assert(1 + Cfg::NC + Cfg::NP <= 16, "named barrier ids");
+  static_assert((Cfg::LSTAGES * 2 + Cfg::QSTAGES * 2 + 5 + kCF + kGroups) * 8 + 4 <= 1024,
                 "barrier area");
 
   const int warp = threadIdx.x >> 5;
@@ -217,8 +235,6 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
     for (int i = 0; i < kGroups; ++i) mbar_init(&g_full[i], 1);
     mbar_init(g_empty, 4);  // drained by 4 warps (one per lane quarter)
     for (int i = 0; i < kCF; ++i) mbar_init(&c_full[i], 1);
-    for (int i = 0; i < Cfg::NC; ++i) mbar_init(&c_empty[i], kGroupWarps);
-    for (int i = 0; i < Cfg::NP; ++i) mbar_init(&p_full[i], kGroupWarps);
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -314,7 +330,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
       for (int j = 0; j < ccnt; ++j, ++i) {
         const uint32_t buf = i % Cfg::NC;
         K8_TL(1, i, 0);
-        if (i >= Cfg::NC) mbar_wait(&c_empty[buf], ((i / Cfg::NC) - 1) & 1);
+        if (i >= Cfg::NC) nbar_sync(1 + buf, (kGroupWarps + 1) * 32);  // C[buf] loaded by its group
         K8_TL(1, i, 1);
         mbar_wait(&x_full[stage], sphase);
         K8_TL(1, i, 2);
@@ -333,7 +349,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
           for (int kk = 0; kk < DP / 16; ++kk)  // + s_lo . hi
             mma_ss_f16_el(d, dal + kk * 2, dxh + kk * 2, IDESC1, 1u);
         }
-        tc_commit_el(&c_full[kGroups == 1 ? buf : i % kGroups]);
+        tc_commit_el(&c_full[kGroups != 4 ? buf : i % kGroups]);
         tc_commit_el(&x_empty[stage]);  // the limbs stage is free once these MMAs complete
         K8_TL(1, i, 3);
         if (++stage == Cfg::LSTAGES) { stage = 0; sphase ^= 1; }
@@ -342,7 +358,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
     }
   } else if (warp == kWarpMma2) {
     // ==================== MMA2 issuer: exact int8 weighted sum ====================
-    // Gq (+)= P[i % NP] . Q once the epilogue group has written the weights (p_full); one commit frees
+    // Gq (+)= P[i % NP] . Q once the epilogue group has written the weights (named barrier); one commit frees
     // the pixel stage and with it the weight buffer (x_empty); at the end of an item hands Gq over.
     constexpr uint32_t IDESC2 = idesc_i8(kBM, Cfg::NQ);
     const uint64_t dq0 = umma_desc(smem_u32(sQ), 16, 1024, 2);  // K-major SW128
@@ -358,7 +374,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
       for (int j = 0; j < ccnt; ++j, ++i) {
         const uint32_t pb = i % Cfg::NP;
         K8_TL(2, i, 0);
-        mbar_wait(&p_full[pb], (i / Cfg::NP) & 1);
+        nbar_sync(1 + Cfg::NC + pb, (kGroupWarps + 1) * 32);  // P[pb] stored by its group
         mbar_wait(&q_full[stage], sphase);
         K8_TL(2, i, 1);
         tc_fence_after();
@@ -421,13 +437,13 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
         const int role = 3 + (grp * kGroupWarps + (warp % kGroupWarps)) % 16;
         (void)role;
         K8_TL(role, ctile, 0);
-        if (kGroups == 1) mbar_wait(&c_full[cb], (ctile / Cfg::NC) & 1);
+        if (kGroups != 4) mbar_wait(&c_full[cb], (ctile / Cfg::NC) & 1);
         else mbar_wait(&c_full[grp], mine & 1);
         ++mine;
         K8_TL(role, ctile, 1);
         tc_fence_after();
         // P[pb] is free once the weighted sum of the tile that used it last has completed
-        // (count-pass tiles too: p_full must not complete twice before MMA2 has seen the first phase)
+        // (count-pass tiles too: without it a group could arrive on P[pb]'s named barrier a phase ahead)
         const uint32_t u = ctile - Cfg::NP;
         const bool need_free = ctile >= (uint32_t)Cfg::NP;
         bool p_free = !need_free;
@@ -437,7 +453,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
         if (!quarter_active) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&c_empty[cb]);
+          K8_RELEASE_C(cb);
           if (!p_free) mbar_wait(&q_empty[u % Cfg::QSTAGES], (u / Cfg::QSTAGES) & 1);
         }
 #pragma unroll
@@ -455,7 +471,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
             K8_TL(role, ctile, 2);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&c_empty[cb]);  // MMA1 may overwrite C[cb]
+            K8_RELEASE_C(cb);  // MMA1 may overwrite C[cb]
           }
           if (!p_free) p_free = mbar_test(&q_empty[u % Cfg::QSTAGES], (u / Cfg::QSTAGES) & 1);
           uint32_t pk[kPart / 4];
@@ -493,7 +509,7 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
         if (w.mode == 0 && !K8_SKIP(16)) tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[pb]);  // MMA2 may consume P[pb]
+        nbar_arrive(1 + Cfg::NC + pb, (kGroupWarps + 1) * 32);  // MMA2 may consume P[pb]
         K8_TL(role, ctile, 5);
         if (ctile == last_tile && h == 0) {
           // ---- drain the item's Gq (this group handled its last tile) into its segment sums ----

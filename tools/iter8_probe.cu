@@ -18,6 +18,8 @@ cudaError_t launch_iter(int DP, const TMaps& tm, const Params& p, int grid, cuda
 cudaError_t launch_iter8(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st);
 cudaError_t setup_iter_attrs();
 cudaError_t setup_iter8_attrs();
+cudaError_t launch_iter9(const TMaps& tm, const Params& p, int grid, cudaStream_t st);
+cudaError_t setup_iter9_attrs();
 }  // namespace fms
 using namespace fms;
 
@@ -73,6 +75,7 @@ int main(int argc, char** argv) {
   const int S_pad = 128 * T_per_frame;
   setup_iter_attrs();
   setup_iter8_attrs();
+  setup_iter9_attrs();
   Params p{};
   p.B = B; p.DP = DP; p.d = DP; p.n = n; p.n_pad = n_pad; p.n_ptiles = (int)(n_pad / 128);
   p.S_pad = S_pad; p.S_cap = S_pad; p.n_chunks = (p.n_ptiles + kChunkTiles - 1) / kChunkTiles;
@@ -120,7 +123,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&p.gacc, (size_t)B * S_pad * DP * 8);
   cudaMalloc(&p.cacc, (size_t)B * S_pad * 4);
   cudaMemset(p.gacc, 0, (size_t)B * S_pad * DP * 8);
-#ifdef K8_TIMELINE
+#if defined(K8_TIMELINE) || defined(K9_TIMELINE)
   cudaMalloc(&p.dbg, 19 * 512 * 8 * 8);
 #endif
   unsigned long long* dclk;
@@ -143,17 +146,22 @@ int main(int argc, char** argv) {
 #ifdef FMS_WAIT_DEBUG
   for (int which = 0; which < 1; ++which) {
 #else
-  for (int which = 0; which < 2; ++which) {
+  for (int which = 0; which < 3; ++which) {
 #endif
-    const int c = which == 0 ? ct : kChunkTiles;
+    if (which == 2 && DP != 16) break;
+    const int c = which != 1 ? ct : kChunkTiles;
     const int nch = (p.n_ptiles + c - 1) / c;
     int cnt[14] = {0};
-    cnt[0] = T * (which == 0 ? nch : p.n_chunks);
+    cnt[0] = T * (which != 1 ? nch : p.n_chunks);
     cnt[1] = T;
     cnt[12] = c;
     cnt[13] = nch;
     cudaMemcpy(p.counters, cnt, sizeof(cnt), cudaMemcpyHostToDevice);
-    auto launch = [&]() { return which == 0 ? launch_iter8(DP, tm, p, 148, 0) : launch_iter(DP, tm, p, 148, 0); };
+    auto launch = [&]() {
+      return which == 0 ? launch_iter8(DP, tm, p, 148, 0)
+                        : which == 1 ? launch_iter(DP, tm, p, 148, 0) : launch_iter9(tm, p, 148, 0);
+    };
+    if (which == 2) cudaMemset(p.gacc, 0, (size_t)B * S_pad * DP * 8);
     for (int w = 0; w < 3; ++w) launch();
     cudaEventRecord(e0);
     const int reps = 10;
@@ -180,9 +188,59 @@ int main(int argc, char** argv) {
     const double ns_tile = ms * 1e6 / tiles_per_sm;
     printf("%s DP=%d B=%d T/frame=%d ct=%d n=%lld: %.3f ms/launch, %.0f ns = %.0f cycles (%.3f GHz) per 128x128 tile per SM, "
            "%.1f TFLOP/s (4nD/pair)\n",
-           which == 0 ? "iter8 (i8 weighted sum)" : "iter  (f16 weighted sum)", DP, B, T_per_frame, c, n, ms, ns_tile,
+           which == 0 ? "iter8 (i8 weighted sum)" : which == 1 ? "iter  (f16 weighted sum)" : "iter9 (two groups)  ", DP, B, T_per_frame, c, n, ms, ns_tile,
            ns_tile * ghz, ghz, pairs * 4 * DP / (ms * 1e-3) / 1e12);
   }
+  if (DP == 16) {
+    // exactness cross-check: one launch of each flat-kernel K2 from zeroed sums, compared bit for bit
+    const int nch = (p.n_ptiles + ct - 1) / ct;
+    int cnt[14] = {0};
+    cnt[0] = T * nch; cnt[1] = T; cnt[12] = ct; cnt[13] = nch;
+    cudaMemcpy(p.counters, cnt, sizeof(cnt), cudaMemcpyHostToDevice);
+    const size_t ng = (size_t)B * S_pad * DP;
+    std::vector<double> g8(ng), g9(ng);
+    cudaMemset(p.gacc, 0, ng * 8);
+    launch_iter8(DP, tm, p, 148, 0);
+    cudaMemcpy(g8.data(), p.gacc, ng * 8, cudaMemcpyDeviceToHost);
+    cudaMemset(p.gacc, 0, ng * 8);
+    launch_iter9(tm, p, 148, 0);
+    cudaMemcpy(g9.data(), p.gacc, ng * 8, cudaMemcpyDeviceToHost);
+    size_t bad = 0, nz = 0;
+    for (size_t i = 0; i < ng; ++i) { bad += g8[i] != g9[i]; nz += g8[i] != 0; }
+    printf("iter9 vs iter8 window sums: %zu of %zu differ (%zu nonzero) %s\n", bad, ng, nz, bad ? "MISMATCH" : "identical");
+  }
+#ifdef K9_TIMELINE
+  {
+    const size_t NE = 19 * 512 * 8;
+    cudaMemset(p.dbg, 0, NE * 8);
+    const int nch = (p.n_ptiles + ct - 1) / ct;
+    int cnt[14] = {0};
+    cnt[0] = T * nch; cnt[1] = T; cnt[12] = ct; cnt[13] = nch;
+    cudaMemcpy(p.counters, cnt, sizeof(cnt), cudaMemcpyHostToDevice);
+    launch_iter9(tm, p, 148, 0);
+    cudaDeviceSynchronize();
+    std::vector<long long> h(NE);
+    cudaMemcpy(h.data(), p.dbg, NE * 8, cudaMemcpyDeviceToHost);
+    auto ev = [&](int role, int t, int e) { return h[((size_t)role * 512 + t) * 8 + e]; };
+    const long long t0 = ev(2, 0, 0);
+    printf("iter9 timeline of CTA 0 (cycles from group 0 warp 0's first wait): k | group g: issuer [C synced, MMA1 issued, "
+           "P synced, MMA2 issued] | warp q0h0 [cfull wait, ld+arrive, alu, pfree wait, st+arrive] | warp q1h1 [same]\n");
+    for (int k = 0; k < 40; ++k) {
+      printf("%3d", k);
+      for (int g = 0; g < 2; ++g) {
+        printf(" | g%d %6lld a%4lld x%4lld i%4lld P%4lld q%4lld i%4lld |", g, ev(g, k, 0) - t0, ev(g, k, 4) - ev(g, k, 0),
+               ev(g, k, 5) - ev(g, k, 4), ev(g, k, 1) - ev(g, k, 5), ev(g, k, 2) - ev(g, k, 1), ev(g, k, 6) - ev(g, k, 2),
+               ev(g, k, 3) - ev(g, k, 6));
+        for (int w : {0, 5}) {
+          const int r = 2 + g * 8 + w;
+          printf(" %6lld[%4lld] %4lld %4lld %4lld %4lld", ev(r, k, 1) - t0, ev(r, k, 1) - ev(r, k, 0), ev(r, k, 2) - ev(r, k, 1),
+                 ev(r, k, 3) - ev(r, k, 2), ev(r, k, 4) - ev(r, k, 3), ev(r, k, 5) - ev(r, k, 4));
+        }
+      }
+      printf("\n");
+    }
+  }
+#endif
 #ifdef K8_TIMELINE
   {
     const size_t NE = 19 * 512 * 8;

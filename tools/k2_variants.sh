@@ -2,7 +2,7 @@
 # K2 probe sweep (run under gpurun): build tools/iter8_probe with compile-time variants and time them.
 # Usage: tools/k2_variants.sh "<nvcc -D flags>;<flags>;..." [probe args]
 set -u
-SRC="tools/iter8_probe.cu paper_2007_14283_b200/csrc/k_iter8.cu paper_2007_14283_b200/csrc/k_iter.cu"
+SRC="tools/iter8_probe.cu paper_2007_14283_b200/csrc/k_iter8.cu paper_2007_14283_b200/csrc/k_iter.cu tools/experiments/k_iter9.cu"
 IFS=';' read -ra VARS <<< "${1:-}"
 shift || true
 i=0
