@@ -4,10 +4,10 @@
 //
 //   prologue:  counters <- 0, K1 prep
 //   WHILE round_cond:                                  OSOP round
-//     K6 select                                        Alg. 2 l.2
+//     K6 select -> plan                                Alg. 2 l.2
 //     step_cond <- 1
 //     WHILE step_cond:                                 lockstep step, Alg. 2 l.4-9
-//       plan -> K2 -> K3 update -> ctl_step -> step_cond_kernel
+//       K2 -> post_step (K3 update, ctl_step, step condition, next plan: k_step.cu)
 //     K4 merge (SMEM sort; IF some pool > 8192: global sort) -> K5 assign -> K7 osop -> round_cond
 //   output centres
 //
@@ -21,15 +21,15 @@ namespace fms {
 
 __global__ void set_cond_kernel(cudaGraphConditionalHandle h, unsigned v) { cudaGraphSetConditional(h, v); }
 
+// the unfused step tail's condition (option fuse_step = 0; post_step_kernel folds it in otherwise)
 __global__ void step_cond_kernel(cudaGraphConditionalHandle h, Params p) {
-  const int steps = ++p.counters[14];
+  ++p.counters[14];
   const int round_steps = ++p.counters[17];
   bool more = p.counters[3] > 0 && p.counters[5] == 0;
   if (more && round_steps > p.max_iter + 2) {
     p.counters[16] = 1;  // the step loop did not terminate
     more = false;
   }
-  (void)steps;
   cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 

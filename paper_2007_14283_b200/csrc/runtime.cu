@@ -34,7 +34,6 @@ cudaError_t launch_iter(int DP, const TMaps& tm, const Params& p, int grid, cuda
 cudaError_t launch_iter8(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st);
 cudaError_t setup_iter8_attrs();
 cudaError_t launch_set_cond(cudaGraphConditionalHandle h, unsigned v, cudaStream_t st);
-cudaError_t launch_step_cond(cudaGraphConditionalHandle h, const Params& p, cudaStream_t st);
 cudaError_t launch_round_cond(cudaGraphConditionalHandle h, const Params& p, cudaStream_t st);
 cudaError_t launch_big_merge_cond(cudaGraphConditionalHandle h, const Params& p, cudaStream_t st);
 cudaError_t launch_merge_small(const Params& p, cudaStream_t st);
@@ -47,6 +46,8 @@ cudaError_t launch_psel(const Params& p, bool pack, cudaStream_t st);
 cudaError_t launch_pstep(const Params& p, bool pack, cudaStream_t st);
 cudaError_t launch_ppost(const Params& p, bool pack, cudaStream_t st);
 cudaError_t launch_update(const Params& p, int num_sms, cudaStream_t st);
+cudaError_t launch_step_cond(cudaGraphConditionalHandle h, const Params& p, cudaStream_t st);
+cudaError_t launch_post_step(cudaGraphConditionalHandle h, const Params& p, int num_sms, cudaStream_t st);
 cudaError_t launch_ctl(const Params& p, cudaStream_t st);
 cudaError_t launch_xchg_pack(const Params& p, cudaStream_t st);
 cudaError_t launch_xkmax(const Params& p, cudaStream_t st);
@@ -117,6 +118,7 @@ struct Ctx {
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr}, ev_done = nullptr;
   // device-resident loop (k_graph.cu): one CUDA graph per call configuration, cached
   int use_graph = 1;             // option "graph"
+  int fuse_step = 0;             // option "fuse_step": the graph's step tail as one kernel (post_step; slower, DESIGN)
   cudaStream_t gst[3] = {nullptr, nullptr, nullptr};  // capture streams (prologue, round body, step body)
   struct GraphEntry {
     cudaGraph_t graph = nullptr;
@@ -312,16 +314,23 @@ fms_status build_graph(Ctx* c, const Params& p, const TMaps& tm, int32_t cap, Ct
     CU(cudaStreamBeginCaptureToGraph(s1, round_body, nullptr, nullptr, 0, mode));
     q = [&]() -> fms_status {
       CU(launch_select(p, c->num_sms, s1));
+      if (c->fuse_step) CU(launch_plan(p, s1));  // the round's first step; post_step plans the next ones
       fms_status q2 = add_cond(s1, &h_step, &step_body, cudaGraphCondTypeWhile);
       if (q2 != FMS_OK) return q2;
       // ---- step body ----
       CU(cudaStreamBeginCaptureToGraph(s2, step_body, nullptr, nullptr, 0, mode));
       q2 = [&]() -> fms_status {
-        CU(launch_plan(p, s2));
-        CU(run_iter(p, tm, c->num_sms, s2));
-        CU(launch_update(p, c->num_sms, s2));
-        CU(launch_ctl(p, s2));
-        CU(launch_step_cond(h_step, p, s2));
+        if (c->fuse_step) {
+          CU(run_iter(p, tm, c->num_sms, s2));
+          // K3 update + ctl_step + the loop condition + the next step's plan in one kernel (k_step.cu)
+          CU(launch_post_step(h_step, p, c->num_sms, s2));
+        } else {
+          CU(launch_plan(p, s2));
+          CU(run_iter(p, tm, c->num_sms, s2));
+          CU(launch_update(p, c->num_sms, s2));
+          CU(launch_ctl(p, s2));
+          CU(launch_step_cond(h_step, p, s2));
+        }
         return FMS_OK;
       }();
       cudaGraph_t gdone = nullptr;
@@ -671,9 +680,10 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
     if (c->h_counters[5]) return fail(c, FMS_E_INTERNAL, "work-item capacity exceeded");
     if (c->h_counters[16]) return fail(c, FMS_E_INTERNAL, "device loop did not terminate");
     steps = c->h_counters[14];
-    // prologue + per round (select 7, set_cond, merge, 3 assign, osop, round_cond) + per step
-    // (plan, K2, update, ctl, step_cond) + output
-    kernels = (p.metric == 1 ? 4 : 2) + 1 + (long long)c->h_counters[15] * 14 + (long long)steps * 5 + (cap > 0);
+    // prologue + per round (select 7, plan, set_cond, merge, 3 assign, osop, round_cond) + per step
+    // (K2, post_step) + output
+    kernels = (p.metric == 1 ? 4 : 2) + 1 + (long long)c->h_counters[15] * (c->fuse_step ? 15 : 14) +
+              (long long)steps * (c->fuse_step ? 2 : 5) + (cap > 0);
   }
 
   fms_status result = FMS_OK;
@@ -979,6 +989,13 @@ fms_status fms_set_option(void* ctx, const char* key, int64_t value) {
   if (!strcmp(key, "graph")) {  // 1: device-resident loop (one CUDA graph launch per call); 0: host-polled
     if (value < 0 || value > 1) return fail(c, FMS_E_INVALID, "graph must be 0 or 1");
     c->use_graph = (int)value;
+    return FMS_OK;
+  }
+  if (!strcmp(key, "fuse_step")) {  // 1: graph step = K2 + post_step; 0: K2 + update + ctl + cond + plan
+    if (value < 0 || value > 1) return fail(c, FMS_E_INVALID, "fuse_step must be 0 or 1");
+    if (c->fuse_step != (int)value)
+      for (auto& e : c->gcache) e.used = 0, e.cap = -1;  // captured graphs no longer match
+    c->fuse_step = (int)value;
     return FMS_OK;
   }
   if (!strcmp(key, "poll_steps")) {  // a frame that finishes idles at most poll_steps - 1 steps

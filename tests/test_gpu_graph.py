@@ -1,7 +1,10 @@
 """The device-resident loop (include/fms.h option "graph", k_graph.cu): one CUDA graph launch per
 call whose round and lockstep-step loops are WHILE conditional nodes must give exactly the results of
 the host-polled loop (same kernels, same order of work per frame), with one host synchronisation per
-call."""
+call.  With option fuse_step = 1 the graph's step tail (K3 update,
+ctl_step, the loop condition, the next plan) is one kernel (post_step_kernel, k_step.cu) whose CTAs
+hand frames and the step over through completion counters; 12 C2 frames exercise that with many
+frames in flight."""
 import numpy as np
 import pytest
 
@@ -18,14 +21,16 @@ def _run(ctx, X, pol, cap=512, **kw):
 
 
 @pytest.mark.parametrize("cfg,seeds,kind", [("S1", [0, 1, 2], 1), ("C1", [3], 0), ("S32sep", [0, 1], 1),
-                                            ("C2", [4], 1)])
-def test_graph_equals_host_loop(cfg, seeds, kind):
+                                            ("C2", [4], 1), ("C2", list(range(10, 22)), 1)])
+@pytest.mark.parametrize("fuse", [0, 1])
+def test_graph_equals_host_loop(cfg, seeds, kind, fuse):
     import paper_2007_14283_b200 as fms
     X = np.stack([synth.make_frame(cfg, s).emb for s in seeds])
     n = X.shape[1]
     pol = (fms.default_policy(kind=0, n_seeds=64) if kind == 0 else
            fms.default_policy(min_instance_px=min_instance_px(n), saturation_stop=1))
     g = fms.Context(0)
+    g.set_option("fuse_step", fuse)
     h = fms.Context(0)
     h.set_option("graph", 0)
     lg, cg, Kg, sg = _run(g, X, pol)
