@@ -491,6 +491,8 @@ def main():
     prof_steps = max(1, min(args.steps, 6))
     ctx.set_option("profile_iter", 1)
     prof_ms_total = 0.0
+    PHASES = ("ms_prep", "ms_select", "ms_step_ctl", "ms_merge", "ms_assign", "ms_host_wait")
+    phase_ms = {key: 0.0 for key in PHASES}
     for k in range(prof_steps):
         e0p, e1p = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0p.record(stream)
@@ -502,6 +504,8 @@ def main():
         totals["iter_seed_iters"] += rs["iter_seed_iters"]
         totals["iter_count_units"] += rs["iter_count_units"]
         totals["iter_launches"] += rs["iter_launches"]
+        for key in PHASES:
+            phase_ms[key] += rs[key]
     ctx.set_option("profile_iter", 0)
 
     # end-to-end through the host-pointer C-ABI entry (H2D + cluster + D2H inside the call)
@@ -539,7 +543,10 @@ def main():
             "flops_per_launch": flops / max(1, totals["iter_launches"]),
             "ms_per_launch": totals["iter_ms"] / max(1, totals["iter_launches"]),
             "iter_share_of_step": totals["iter_ms"] / prof_ms_total if prof_ms_total > 0 else None,
-            "measured": f"separate profiled pass of {prof_steps} step(s) after the timed region"}
+            "measured": f"separate profiled pass of {prof_steps} step(s) after the timed region",
+            # the rest of the profiled steps by phase (device time per step, host-polled loop)
+            "phase_ms_per_step": {"K2": totals["iter_ms"] / prof_steps,
+                                  **{k[3:]: v / prof_steps for k, v in phase_ms.items()}}}
     # frame-level roofline: algorithmic iteration FLOPs of the whole timed job at the tensor peak (the
     # K2 launches' work of the timed steps: seed-iterations of every frame)
     job_iter_flops = totals["seed_iters"] * n * 4 * d

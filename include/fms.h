@@ -90,6 +90,11 @@ typedef struct {
   int64_t iter_count_units;   /* sum over K2 launches of converged modes counted (intensity pass, R10) */
   int64_t host_syncs;         /* host waits on the stream during the call: 1 with the device-resident loop
                                  (option "graph", the default); one per poll with the host-polled loop */
+  /* per-phase device time (ms), only with option "profile_iter" = 1 (the host-polled loop; events at the
+     phase boundaries on the call's stream): K1 prep; K6 selection; the per-step control around K2
+     (plan, K3 update, ctl_step, and the seed-sharding step exchange); K4 merge; K5 assignment + K7 OSOP;
+     the stream idle while the host polls.  K2 itself is iter_ms. */
+  double ms_prep, ms_select, ms_step_ctl, ms_merge, ms_assign, ms_host_wait;
 } fms_run_stats;
 
 fms_status fms_default_policy(fms_seed_policy* out);

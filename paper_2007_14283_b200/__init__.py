@@ -60,7 +60,9 @@ class RunStats(C.Structure):
     _fields_ = [("ms_total", C.c_double), ("workspace_bytes", C.c_int64), ("steps", C.c_int32),
                 ("iter_launches", C.c_int32), ("iter_ms", C.c_double), ("iter_seed_iters", C.c_int64),
                 ("iter_items", C.c_int64), ("launches", C.c_int64), ("iter_count_units", C.c_int64),
-                ("host_syncs", C.c_int64)]
+                ("host_syncs", C.c_int64), ("ms_prep", C.c_double), ("ms_select", C.c_double),
+                ("ms_step_ctl", C.c_double), ("ms_merge", C.c_double), ("ms_assign", C.c_double),
+                ("ms_host_wait", C.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

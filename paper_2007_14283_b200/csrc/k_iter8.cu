@@ -67,7 +67,11 @@ struct Iter8Cfg {
 #endif
   // 32-lane rows: a drain adds its sums straight to the global accumulator (fp64 atomics of exact
   // integers) instead of shared-memory segment sums, which leaves room for a deeper pixel ring
+#ifdef K8_DIRECT_ALL
+  static constexpr bool DIRECT = true;
+#else
   static constexpr bool DIRECT = DP == 32;
+#endif
   static constexpr int GROUP_WARPS = k8::kEpiWarps / GROUPS;  // a multiple of 4 (one per lane quarter)
   // 4 groups of 4 warps (the default) or 1 group of 16 warps (every warp on every tile, 32 columns
   // each: 16 TMEM loads in flight per tile; measured slower, 906 vs 805 cycles per tile).  2 groups
@@ -107,8 +111,13 @@ struct Iter8Cfg {
   // Two rings: the limbs (MMA1's B operand) free a stage when MMA1 is done with it; the digit planes
   // (MMA2's B) when MMA2 is.  A stage of the limb ring is held for a few hundred cycles, so the ring
   // prefetches far ahead of the similarity MMAs for its size.
+#if defined(K8_LSTAGES) && defined(K8_QSTAGES)
+  static constexpr int LSTAGES = DP == 16 ? K8_LSTAGES : 5;
+  static constexpr int QSTAGES = DP == 16 ? K8_QSTAGES : 8;
+#else
   static constexpr int LSTAGES = DP == 16 ? 8 : 5;
   static constexpr int QSTAGES = DP == 16 ? 10 : 8;
+#endif
   static constexpr int GS_B = DIRECT ? 0 : kBM * DP * 8;  // int64 segment sums, [DP][kBM], per group
   static constexpr int SMEM = 1024 + 6 * A_B + LSTAGES * L_B + QSTAGES * Q_B + GROUPS * GS_B + 1024;
   static_assert(SMEM <= 232448, "shared memory");

@@ -91,6 +91,10 @@ struct Ctx {
   size_t h_ctl_cap = 0;
   // profiling
   std::vector<cudaEvent_t> ev;
+  // per-phase timing (profile_iter): an event at every phase boundary of the host-polled loop; the
+  // time to the next mark belongs to the mark's phase (fms_run_stats.ms_prep ... ms_host_wait)
+  std::vector<cudaEvent_t> pev;
+  std::vector<int> pev_phase;
   int* h_prof = nullptr;   // per launch: counters[0..kProfInts) snapshot
   size_t h_prof_cap = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -491,6 +495,20 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   // and step loops on the device (k_graph.cu); sharded calls (a collective between kernels) and
   // profiled calls run the host-polled loop below
   const bool gmode = c->use_graph && !pshard && p.world == 1 && !c->profile;
+  enum { PHASE_PREP, PHASE_SELECT, PHASE_ITER, PHASE_STEP, PHASE_MERGE, PHASE_ASSIGN, PHASE_HOST, PHASE_END };
+  int nmarks = 0;
+  auto mark = [&](int phase) -> cudaError_t {  // profiled host loop only
+    if (!c->profile) return cudaSuccess;
+    if ((int)c->pev.size() <= nmarks) {
+      cudaEvent_t e;
+      cudaError_t err = cudaEventCreate(&e);
+      if (err != cudaSuccess) return err;
+      c->pev.push_back(e);
+      c->pev_phase.push_back(0);
+    }
+    c->pev_phase[nmarks] = phase;
+    return cudaEventRecord(c->pev[nmarks++], st);
+  };
   int steps = 0, launches = 0;
   long long kernels = 2;  // init + prep
   long long syncs = 0;    // host waits on the stream during the call
@@ -542,6 +560,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
       fms_status g = pgrow(std::max<size_t>(post_ints, B));
       if (g != FMS_OK) return g;
     }
+    CU(mark(PHASE_PREP));
     CU(launch_prep(p, st));
     if (pshard) {  // a zero-norm row on any rank fails the frame on every rank
       CU(launch_pstat(p, true, st));
@@ -550,10 +569,12 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
       CU(launch_pstat(p, false, st));
     }
     for (int round = 0; round < pol->max_rounds + 1; ++round) {
+      CU(mark(PHASE_SELECT));
       CU(launch_select(p, c->num_sms, st));
       kernels += 7;
       if (pshard) {  // the round's seed rows come from the ranks holding the seed pixels
         CU(launch_psel_kmax(p, st));
+        CU(mark(PHASE_HOST));
         CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
         ++syncs;
@@ -571,6 +592,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
       }
       for (int s = 0; s < max_iters + c->poll; s += c->poll) {
         for (int k = 0; k < c->poll; ++k) {
+          CU(mark(PHASE_STEP));
           CU(launch_plan(p, st));
           if (c->profile) {
             const size_t slot = launches;
@@ -594,9 +616,11 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
               c->h_prof = np;
               c->h_prof_cap = ncap;
             }
+            CU(mark(PHASE_ITER));
             CU(cudaEventRecord(c->ev[2 * slot], st));
             CU(run_iter(p, tm, c->num_sms, st));
             CU(cudaEventRecord(c->ev[2 * slot + 1], st));
+            CU(mark(PHASE_STEP));
             CU(cudaMemcpyAsync(c->h_prof + slot * kProfInts, p.counters, kProfInts * sizeof(int), cudaMemcpyDeviceToHost,
                                st));
             ++launches;
@@ -619,14 +643,17 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
           ++steps;
           kernels += p.world > 1 ? 5 : 4;  // plan, iter, update, (exchange pack), ctl_step
         }
+        CU(mark(PHASE_HOST));
         CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
         ++syncs;
         if (c->h_counters[5]) return fail(c, FMS_E_INTERNAL, "work-item capacity exceeded");
         if (c->h_counters[3] == 0) break;  // no frame still iterating
       }
+      CU(mark(PHASE_MERGE));
       if (p.world > 1) {  // seed sharding: every rank gets every owner's converged seeds before the merge
         CU(launch_xkmax(p, st));
+        CU(mark(PHASE_HOST));
         CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
         ++syncs;
@@ -647,9 +674,11 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
         }
         kernels += 1;
       }
+      CU(mark(PHASE_MERGE));
       CU(launch_merge_small(p, st));
       // the global-memory merge only when a pool exceeds the SMEM sort (the last poll read counters[18])
       if (p.P_cap > kMaxPcap && c->h_counters[18] > kMaxPcap) CU(launch_merge_big(p, st));
+      CU(mark(PHASE_ASSIGN));
       CU(launch_assign_osop(p, tm, c->num_sms, st, !pshard));
       kernels += 5;  // merge, assign (tensor cores, <= 128 and <= 256 centres), assign (CUDA cores), osop
       if (pshard) {  // histogram, candidate count and coverage over all pixels before the OSOP step
@@ -660,11 +689,13 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
         CU(launch_osop(p, st));
         kernels += 2;
       }
+      CU(mark(PHASE_HOST));
       CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
       CU(cudaStreamSynchronize(st));
-        ++syncs;
+      ++syncs;
       if (c->h_counters[2] == 0) break;  // every frame DONE (or in error)
     }
+    CU(mark(PHASE_ASSIGN));
     if (cap > 0) {
       CU(launch_output(p, centres, cap, st));
       kernels += 1;
@@ -743,6 +774,13 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
         rs->iter_items += snap[0];
         rs->iter_seed_iters += reinterpret_cast<const long long*>(snap + 6)[0];
         rs->iter_count_units += reinterpret_cast<const long long*>(snap + 10)[0];
+      }
+      double* ph[PHASE_END] = {&rs->ms_prep, &rs->ms_select, nullptr, &rs->ms_step_ctl, &rs->ms_merge,
+                               &rs->ms_assign, &rs->ms_host_wait};
+      for (int i = 0; i < nmarks; ++i) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, c->pev[i], i + 1 < nmarks ? c->pev[i + 1] : c->t1);
+        if (ph[c->pev_phase[i]]) *ph[c->pev_phase[i]] += t;
       }
     }
   }
@@ -854,6 +892,7 @@ void fms_ctx_destroy(void* ctx) {
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->cstream) cudaStreamDestroy(c->cstream);
   for (auto e : c->ev) cudaEventDestroy(e);
+  for (auto e : c->pev) cudaEventDestroy(e);
   for (auto& e : c->gcache) {
     if (e.exec) cudaGraphExecDestroy(e.exec);
     if (e.graph) cudaGraphDestroy(e.graph);

@@ -67,3 +67,26 @@ def test_graph_euclid_and_host_entry_chunks():
         co = torch.zeros((5, 512, X.shape[2]), dtype=torch.float32).pin_memory()
         _, K, rs = g.cluster_host(eh, lo, co, 512, h=(0.2) ** 0.5, policy=pol)
         assert K == Kg and np.array_equal(lo.numpy(), lg) and np.array_equal(co.numpy(), cg)
+
+
+def test_phase_times_profiled_loop():
+    """fms_run_stats per-phase device times (option profile_iter, host-polled loop): every phase that
+    ran has time, and the phases plus K2 account for the call's stream time."""
+    import paper_2007_14283_b200 as fms
+    X = np.stack([synth.make_frame("C2", s).emb for s in (30, 31, 32)])
+    pol = fms.default_policy(min_instance_px=min_instance_px(X.shape[1]), saturation_stop=1)
+    ctx = fms.Context(0)
+    ctx.set_option("profile_iter", 1)
+    _run(ctx, X, pol)  # warm-up (workspace, events)
+    _, _, _, st = _run(ctx, X, pol)
+    r = st["run"]
+    for k in ("ms_prep", "ms_select", "ms_step_ctl", "ms_merge", "ms_assign", "iter_ms"):
+        assert r[k] > 0, (k, r)
+    parts = r["iter_ms"] + sum(r[k] for k in ("ms_prep", "ms_select", "ms_step_ctl", "ms_merge", "ms_assign",
+                                              "ms_host_wait"))
+    assert abs(parts - r["ms_total"]) <= 0.05 * r["ms_total"] + 0.05, (parts, r["ms_total"])
+    assert r["iter_ms"] > r["ms_step_ctl"]
+    # without profiling the graph path leaves them at zero
+    ctx.set_option("profile_iter", 0)
+    _, _, _, st = _run(ctx, X, pol)
+    assert st["run"]["ms_select"] == 0 and st["run"]["host_syncs"] == 1
