@@ -85,7 +85,7 @@ __device__ void plan_body(const Params& p, int* sm, int* s_tiles_total_p) {
       long long per_cta = total / (32ll * p.num_sms);
       per_cta = per_cta < 1 ? 1 : (per_cta > 8 ? 8 : per_cta);
       const long long want = (total + per_cta * p.num_sms - 1) / (per_cta * p.num_sms);
-      const long long cmax = p.DP == 16 ? kChunkMax : kChunkMax / 2;  // 28 KB tiles at DP = 32
+      const long long cmax = p.DP == 16 ? p.item_tiles_max : p.item_tiles_max / 2;  // 28 KB tiles at DP = 32
       ct = (int)(want < 1 ? 1 : (want > cmax ? cmax : want));
       if (ct > p.n_ptiles) ct = p.n_ptiles;
       nch = (p.n_ptiles + ct - 1) / ct;

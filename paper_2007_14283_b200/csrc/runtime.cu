@@ -450,6 +450,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   p.emb = emb;
   p.labels = labels;
   p.num_sms = c->num_sms;
+  p.item_tiles_max = kChunkMax;  // r2: 16 / 32 / 48 / 64 tiles measured 1622 / 1720 / 1678 / 1625 frames/s
 
   const size_t need = carve(p, nullptr);
   if (need > c->ws_bytes) {
