@@ -288,8 +288,13 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
             mbar_arrive(&x_full[stage]);
           } else {
             mbar_expect_tx(&x_full[stage], Cfg::L_B);
+#ifdef K8_BULK_LIMBS  // timing experiment: contiguous 1-D copies (wrong smem layout for the MMA)
+            bulk_load(st, p.Xh + (size_t)xrow * DP, Cfg::TILE_B, &x_full[stage]);
+            bulk_load(st + Cfg::TILE_B, p.Xl + (size_t)xrow * DP, Cfg::TILE_B, &x_full[stage]);
+#else
             tma_load_2d(st, &tm.xh, &x_full[stage], 0, xrow);
             tma_load_2d(st + Cfg::TILE_B, &tm.xl, &x_full[stage], 0, xrow);
+#endif
           }
         }
         __syncwarp();
@@ -313,7 +318,11 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
             mbar_arrive(&q_full[stage]);
           } else {
             mbar_expect_tx(&q_full[stage], Cfg::Q_B);
+#ifdef K8_BULK_DIGITS  // timing experiment: contiguous 1-D copy (wrong smem layout for the MMA)
+            bulk_load(sQ + stage * Cfg::Q_B, p.Xq + (size_t)(tile0 + j) * Cfg::Q_B, Cfg::Q_B, &q_full[stage]);
+#else
             tma_load_2d(sQ + stage * Cfg::Q_B, &tm.xq, &q_full[stage], 0, (int)((tile0 + j) * Cfg::NQ));
+#endif
           }
         }
         __syncwarp();

@@ -85,6 +85,7 @@ int main(int argc, char** argv) {
   int8_t* xq;
   cudaMalloc(&xh, B * n_pad * DP * 2); cudaMalloc(&xl, B * n_pad * DP * 2);
   cudaMalloc(&xq, B * n_pad * DP * 3);
+  p.Xh = xh; p.Xl = xl; p.Xq = xq;  // raw pointers (the bulk-copy timing experiments read them)
   cudaMalloc(&sh, B * S_pad * DP * 2); cudaMalloc(&ss, B * S_pad * DP * 2); cudaMalloc(&sl, B * S_pad * DP * 2);
   // pixels: half of them near the seed direction (in window), half far -- the epilogue cost does not
   // depend on the data, the window sums just need to be non-trivial
