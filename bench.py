@@ -52,6 +52,7 @@ def parse():
                     help="euclid (NEXT-4, reading R24): the C2 frames row-normalised, Euclidean window "
                          "sqrt(2h) (the same windows as cosine h at the start), window-mean update")
     ap.add_argument("--host-chunk", type=int, default=0, help="e2e: frames per host-entry chunk (0 = library default)")
+    ap.add_argument("--no-pdl", action="store_true", help="launch the step kernels without programmatic dependent launch")
     ap.add_argument("--fuse-step", type=int, default=0, choices=[0, 1],
                     help="graph step tail as one kernel (1; measured slower) or update / ctl / cond / plan kernels (0, default)")
     ap.add_argument("--extras-budget-s", type=float, default=300.0,
@@ -457,6 +458,8 @@ def main():
         ctx.set_option("host_chunk", args.host_chunk)
     if args.fuse_step:
         ctx.set_option("fuse_step", args.fuse_step)
+    if args.no_pdl:
+        ctx.set_option("pdl", 0)
     pol = fms.default_policy(**policy_kwargs(n))
     stream = torch.cuda.current_stream(dev)
 

@@ -183,7 +183,10 @@ fms_status fms_ctx_create_dist(void** ctx_out, int device, const void* unique_id
 fms_status fms_set_pixel_shard(void* ctx, fms_exchange_fn fn, void* user, int32_t rank, int32_t world,
                                int64_t n_global, int64_t offset);
 
-/* Options: "graph" (0/1, default 1): run a single-GPU call as one CUDA graph launch whose round and
+/* Options: "pdl" (0/1, default 1): launch the lockstep-step kernels (plan, K2, K3 update, ctl_step, the
+ *          step condition) with programmatic dependent launch, so each one's launch and prologue
+ *          overlap its predecessor's tail (off in profiled calls).
+ *          "graph" (0/1, default 1): run a single-GPU call as one CUDA graph launch whose round and
  *          lockstep-step loops are WHILE conditional nodes with device-set conditions (one host
  *          synchronisation per call); sharded and profiled calls always use the host-polled loop.
  *          "profile_iter" (0/1): time every K2 launch with CUDA events for fms_run_stats.iter_ms

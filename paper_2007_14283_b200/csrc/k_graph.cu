@@ -23,6 +23,7 @@ __global__ void set_cond_kernel(cudaGraphConditionalHandle h, unsigned v) { cuda
 
 // the unfused step tail's condition (option fuse_step = 0; post_step_kernel folds it in otherwise)
 __global__ void step_cond_kernel(cudaGraphConditionalHandle h, Params p) {
+  pdl_wait();
   ++p.counters[14];
   const int round_steps = ++p.counters[17];
   bool more = p.counters[3] > 0 && p.counters[5] == 0;
@@ -58,8 +59,7 @@ cudaError_t launch_set_cond(cudaGraphConditionalHandle h, unsigned v, cudaStream
   return cudaGetLastError();
 }
 cudaError_t launch_step_cond(cudaGraphConditionalHandle h, const Params& p, cudaStream_t st) {
-  step_cond_kernel<<<1, 1, 0, st>>>(h, p);
-  return cudaGetLastError();
+  return launch_ex(p.pdl, step_cond_kernel, 1, 1, 0, st, h, p);
 }
 cudaError_t launch_round_cond(cudaGraphConditionalHandle h, const Params& p, cudaStream_t st) {
   round_cond_kernel<<<1, 1, 0, st>>>(h, p);

@@ -143,6 +143,7 @@ __device__ __forceinline__ ItemDesc item_desc(const Params& p, int item) {
 template <int DP, bool GAUSS>
 __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_constant__ TMaps tm, Params p) {
   using Cfg = IterCfg<DP>;
+  pdl_wait();
   const int n_items = p.counters[0];
   // equal contiguous item ranges per CTA
   const int i_begin = (int)(((long long)n_items * blockIdx.x) / gridDim.x);
@@ -470,13 +471,12 @@ int iter_smem_bytes(int DP) { return DP == 16 ? IterCfg<16>::SMEM : IterCfg<32>:
 cudaError_t launch_iter(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st) {
   const bool g = p.profile == 1;
   if (DP == 16) {
-    if (g) iter_kernel<16, true><<<grid, kIterThreads, IterCfg<16>::SMEM, st>>>(tm, p);
-    else iter_kernel<16, false><<<grid, kIterThreads, IterCfg<16>::SMEM, st>>>(tm, p);
+    return launch_ex(p.pdl, g ? iter_kernel<16, true> : iter_kernel<16, false>, grid, kIterThreads, IterCfg<16>::SMEM,
+                     st, tm, p);
   } else {
-    if (g) iter_kernel<32, true><<<grid, kIterThreads, IterCfg<32>::SMEM, st>>>(tm, p);
-    else iter_kernel<32, false><<<grid, kIterThreads, IterCfg<32>::SMEM, st>>>(tm, p);
+    return launch_ex(p.pdl, g ? iter_kernel<32, true> : iter_kernel<32, false>, grid, kIterThreads, IterCfg<32>::SMEM,
+                     st, tm, p);
   }
-  return cudaGetLastError();
 }
 
 cudaError_t setup_iter_attrs() {

@@ -195,13 +195,6 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
   using Cfg = Iter8Cfg<DP>;
   constexpr int kGroups = Cfg::GROUPS, kGroupWarps = Cfg::GROUP_WARPS;
   constexpr int kColsPerWarp = Cfg::COLS_PER_WARP, kParts = Cfg::PARTS, kPart = Cfg::PART;
-  const int n_items = p.counters[0];
-  const int ct = p.counters[12];   // pixel tiles per work item
-  const int nch = p.counters[13];  // work items per seed tile
-  const int i_begin = (int)(((long long)n_items * blockIdx.x) / gridDim.x);
-  const int i_end = (int)(((long long)n_items * (blockIdx.x + 1)) / gridDim.x);
-  if (i_begin >= i_end) return;
-
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                    // [2 buffers][s_hi, s_hs, s_lo][A_B]
@@ -257,7 +250,17 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  if (warp == kWarpTma) {
+  // everything above (barriers, descriptor prefetch, TMEM) overlaps the predecessor under PDL; the
+  // work list below is its output
+  pdl_wait();
+  const int n_items = p.counters[0];
+  const int ct = p.counters[12];   // pixel tiles per work item
+  const int nch = p.counters[13];  // work items per seed tile
+  const int i_begin = (int)(((long long)n_items * blockIdx.x) / gridDim.x);
+  const int i_end = (int)(((long long)n_items * (blockIdx.x + 1)) / gridDim.x);
+  if (i_begin >= i_end) {
+    // no work: nothing to do but release TMEM below
+  } else if (warp == kWarpTma) {
     // ================================ TMA producer ================================
     int xi = 0;
     int stage = 0;
@@ -590,9 +593,8 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
 int iter8_smem_bytes(int DP) { return DP == 16 ? Iter8Cfg<16>::SMEM : Iter8Cfg<32>::SMEM; }
 
 cudaError_t launch_iter8(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st) {
-  if (DP == 16) iter8_kernel<16><<<grid, k8::kThreads, Iter8Cfg<16>::SMEM, st>>>(tm, p);
-  else iter8_kernel<32><<<grid, k8::kThreads, Iter8Cfg<32>::SMEM, st>>>(tm, p);
-  return cudaGetLastError();
+  if (DP == 16) return launch_ex(p.pdl, iter8_kernel<16>, grid, k8::kThreads, Iter8Cfg<16>::SMEM, st, tm, p);
+  return launch_ex(p.pdl, iter8_kernel<32>, grid, k8::kThreads, Iter8Cfg<32>::SMEM, st, tm, p);
 }
 
 cudaError_t setup_iter8_attrs() {

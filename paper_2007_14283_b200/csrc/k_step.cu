@@ -104,6 +104,7 @@ __device__ void plan_body(const Params& p, int* sm, int* s_tiles_total_p) {
 __global__ void plan_kernel(Params p) {
   __shared__ int sm[33];
   __shared__ int s_tiles_total;
+  pdl_wait();
   plan_body<false>(p, sm, &s_tiles_total);
 }
 
@@ -189,6 +190,7 @@ __device__ void update_tile(const Params& p, const TileTask& task) {
 
 template <int DP>
 __global__ void __launch_bounds__(kBM) update_kernel(Params p) {
+  pdl_wait();
   const int n_tiles = p.counters[1];
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) update_tile<DP, false>(p, p.tiles[t]);
 }
@@ -295,6 +297,7 @@ template <int DP>
 __global__ void ctl_step_kernel(Params p) {
   __shared__ int s_end, s_rem;
   __shared__ int sm[33];
+  pdl_wait();
   ctl_frame<DP, false>(p, blockIdx.x, sm, s_end, s_rem);
 }
 
@@ -501,8 +504,7 @@ cudaError_t launch_xround(const Params& p, bool pack, cudaStream_t st) {
 }
 
 cudaError_t launch_plan(const Params& p, cudaStream_t st) {
-  plan_kernel<<<1, 1024, 0, st>>>(p);
-  return cudaGetLastError();
+  return launch_ex(p.pdl, plan_kernel, 1, 1024, 0, st, p);
 }
 
 cudaError_t launch_post_step(cudaGraphConditionalHandle h, const Params& p, int num_sms, cudaStream_t st) {
@@ -512,14 +514,11 @@ cudaError_t launch_post_step(cudaGraphConditionalHandle h, const Params& p, int 
 }
 
 cudaError_t launch_update(const Params& p, int num_sms, cudaStream_t st) {
-  if (p.DP == 16) update_kernel<16><<<num_sms, kBM, 0, st>>>(p);  // grid-stride over the step's tiles
-  else update_kernel<32><<<num_sms, kBM, 0, st>>>(p);
-  return cudaGetLastError();
+  // grid-stride over the step's tiles
+  return launch_ex(p.pdl, p.DP == 16 ? update_kernel<16> : update_kernel<32>, num_sms, kBM, 0, st, p);
 }
 cudaError_t launch_ctl(const Params& p, cudaStream_t st) {
-  if (p.DP == 16) ctl_step_kernel<16><<<p.B, 256, 0, st>>>(p);
-  else ctl_step_kernel<32><<<p.B, 256, 0, st>>>(p);
-  return cudaGetLastError();
+  return launch_ex(p.pdl, p.DP == 16 ? ctl_step_kernel<16> : ctl_step_kernel<32>, p.B, 256, 0, st, p);
 }
 
 }  // namespace fms

@@ -122,6 +122,7 @@ struct Ctx {
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr}, ev_done = nullptr;
   // device-resident loop (k_graph.cu): one CUDA graph per call configuration, cached
   int use_graph = 1;             // option "graph"
+  int pdl = 1;                   // option "pdl": programmatic dependent launch of the step-loop kernels
   int fuse_step = 0;             // option "fuse_step": the graph's step tail as one kernel (post_step; slower, DESIGN)
   cudaStream_t gst[3] = {nullptr, nullptr, nullptr};  // capture streams (prologue, round body, step body)
   struct GraphEntry {
@@ -450,7 +451,8 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   p.emb = emb;
   p.labels = labels;
   p.num_sms = c->num_sms;
-  p.item_tiles_max = kChunkMax;  // r2: 16 / 32 / 48 / 64 tiles measured 1622 / 1720 / 1678 / 1625 frames/s
+  p.item_tiles_max = kChunkMax;
+  p.pdl = c->pdl && !c->profile;  // profiled calls time K2 with events between plain launches  // r2: 16 / 32 / 48 / 64 tiles measured 1622 / 1720 / 1678 / 1625 frames/s
 
   const size_t need = carve(p, nullptr);
   if (need > c->ws_bytes) {
@@ -1029,6 +1031,11 @@ fms_status fms_set_option(void* ctx, const char* key, int64_t value) {
   if (!strcmp(key, "graph")) {  // 1: device-resident loop (one CUDA graph launch per call); 0: host-polled
     if (value < 0 || value > 1) return fail(c, FMS_E_INVALID, "graph must be 0 or 1");
     c->use_graph = (int)value;
+    return FMS_OK;
+  }
+  if (!strcmp(key, "pdl")) {  // 1: plan / K2 / update / ctl_step / step condition launched with PDL
+    if (value < 0 || value > 1) return fail(c, FMS_E_INVALID, "pdl must be 0 or 1");
+    c->pdl = (int)value;
     return FMS_OK;
   }
   if (!strcmp(key, "fuse_step")) {  // 1: graph step = K2 + post_step; 0: K2 + update + ctl + cond + plan
