@@ -49,6 +49,18 @@ constexpr int kColsPerWarp = kBN / 2;
 constexpr int kWarpTma = kEpiWarps, kWarpMma1 = kEpiWarps + 1, kWarpMma2 = kEpiWarps + 2;
 constexpr int kIterThreads = (kEpiWarps + 3) * 32;
 
+// Epilogue -> issuer hand-offs as named barriers (as in k_iter8.cu: one per C buffer, ids 1..NC, and
+// one per weight buffer, ids NC + 1..NC + NP; a group's next arrival on one needs an MMA the waiting
+// warp issues only after its sync); -DK2_MBAR_HANDOFF restores the mbarrier hand-offs
+#ifdef K2_MBAR_HANDOFF
+#define K2_RELEASE_C(b)                          \
+  do {                                           \
+    if (lane == 0) mbar_arrive(&c_empty[(b)]);   \
+  } while (0)
+#else
+#define K2_RELEASE_C(b) nbar_arrive(1 + (int)(b), (kGroupWarps + 1) * 32)
+#endif
+
 template <int DP>
 struct IterCfg {
   static constexpr int ROW_B = DP * 2;                    // bytes per row (fp16)
@@ -256,7 +268,11 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
       for (int j = 0; j < ccnt; ++j, ++i) {
         const uint32_t buf = i % Cfg::NC;
         tlog(p, 1, i, 0);
+#ifdef K2_MBAR_HANDOFF
         if (i >= Cfg::NC) role_wait(&c_empty[buf], ((i / Cfg::NC) - 1) & 1);
+#else
+        if (i >= Cfg::NC) nbar_sync(1 + buf, (kGroupWarps + 1) * 32);  // C[buf] loaded by its group
+#endif
         tlog(p, 1, i, 1);
         role_wait(&x_full[stage], sphase);
         tlog(p, 1, i, 2);
@@ -300,7 +316,11 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
       const uint32_t g_tmem = tmem + Cfg::G_COL + ab * Cfg::G_N;
       for (int j = 0; j < ccnt; ++j, ++i) {
         const uint32_t pb = i % Cfg::NP;
+#ifdef K2_MBAR_HANDOFF
         role_wait(&p_full[pb], (i / Cfg::NP) & 1);
+#else
+        nbar_sync(1 + Cfg::NC + pb, (kGroupWarps + 1) * 32);  // P[pb] stored by its group
+#endif
         tc_fence_after();
         if (w.mode == 0 && !K2_OFF(p, 1)) {
           const uint64_t bd0 = dxg0 + (uint64_t)(stage * (2 * Cfg::TILE_B >> 4));
@@ -399,14 +419,14 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         const uint32_t pb = ctile % Cfg::NP;
         tc_fence_after();
         uint32_t v[kColsPerWarp];
-        if (K2_OFF(p, 128) && lane == 0) mbar_arrive(&c_empty[grp]);  // timing experiment: release early
+        if (K2_OFF(p, 128)) K2_RELEASE_C(grp);  // timing experiment: release early
         if (!K2_OFF(p, 16)) {
           tmem_ld64(cbase, v);  // one instruction: the scheduler cannot interleave math between pieces
           tmem_ld_wait();
         }
         tc_fence_before();
         __syncwarp();
-        if (!K2_OFF(p, 128) && lane == 0) mbar_arrive(&c_empty[grp]);  // MMA1 may overwrite C[grp]
+        if (!K2_OFF(p, 128)) K2_RELEASE_C(grp);  // MMA1 may overwrite C[grp]
         tlog(p, lrole, ctile, 2);
         // P[pb] is free once the weighted sum of the tile that used it last has completed: probe
         // now, use the answer after the flat kernel
@@ -440,7 +460,11 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         tlog(p, lrole, ctile, 3);
         tc_fence_before();
         __syncwarp();
+#ifdef K2_MBAR_HANDOFF
         if (lane == 0) mbar_arrive(&p_full[pb]);  // MMA2 may consume P[pb]
+#else
+        nbar_arrive(1 + Cfg::NC + pb, (kGroupWarps + 1) * 32);  // MMA2 may consume P[pb]
+#endif
         tlog(p, lrole, ctile, 4);
         ++mine;
         if (drainer && pend >= 0) { drain(pend, pend_it); pend = -1; }
