@@ -510,6 +510,15 @@ def main():
         for key in PHASES:
             phase_ms[key] += rs[key]
     ctx.set_option("profile_iter", 0)
+    # guard pairs: one step with the counting K2 instantiation -- the lockstep window
+    # decisions within the similarity's certified error bound of tau (not certified against the
+    # exact similarity), per frame and as a fraction of the pairs evaluated
+    ctx.set_option("guard_stats", 1)
+    gfs, grs = step(0)
+    ctx.set_option("guard_stats", 0)
+    g_pairs_eval = sum(f["seed_iters"] for f in gfs) * n
+    guard = {"per_frame": grs["guard_pairs"] / B, "fraction_of_pairs": grs["guard_pairs"] / max(1, g_pairs_eval),
+             "eps": 2.0 ** -16, "frames": B}
 
     # end-to-end through the host-pointer C-ABI entry (H2D + cluster + D2H inside the call)
     e2e = None
@@ -609,6 +618,7 @@ def main():
                    "frames_per_step": B, "l2": "2 alternating input batches of B x 16 MiB (> 126 MB L2)",
                    "parallelism": f"seed-sharded x{world} ({args.backend})" if sharded else f"replicas x{world}"},
         "roofline": roof,
+        "guard_pairs": guard,
         "frame_level_frac": frame_roof_ms / ms if ms > 0 else None,
         "job_roofline": roof_terms,
         "seed_iters_per_frame": totals["seed_iters"] / max(1, totals["frames"]),

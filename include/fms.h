@@ -95,6 +95,10 @@ typedef struct {
      (plan, K3 update, ctl_step, and the seed-sharding step exchange); K4 merge; K5 assignment + K7 OSOP;
      the stream idle while the host polls.  K2 itself is iter_ms. */
   double ms_prep, ms_select, ms_step_ctl, ms_merge, ms_assign, ms_host_wait;
+  /* with option "guard_stats" = 1: lockstep-iteration (seed, pixel) pairs whose computed similarity lay
+     within 2^-16 of tau -- the certified error bound of the 3-term fp32 similarity -- i.e. the window
+     decisions (Eq. 11) the CUDA path cannot certify against the exact similarity; 0 otherwise */
+  int64_t guard_pairs;
 } fms_run_stats;
 
 fms_status fms_default_policy(fms_seed_policy* out);
@@ -183,7 +187,9 @@ fms_status fms_ctx_create_dist(void** ctx_out, int device, const void* unique_id
 fms_status fms_set_pixel_shard(void* ctx, fms_exchange_fn fn, void* user, int32_t rank, int32_t world,
                                int64_t n_global, int64_t offset);
 
-/* Options: "pdl" (0/1, default 1): launch the lockstep-step kernels (plan, K2, K3 update, ctl_step, the
+/* Options: "guard_stats" (0/1, default 0): count the uncertified window decisions (fms_run_stats.guard_pairs)
+ *          with a K2 instantiation that tests every pair against the similarity's error bound.
+ *          "pdl" (0/1, default 1): launch the lockstep-step kernels (plan, K2, K3 update, ctl_step, the
  *          step condition) with programmatic dependent launch, so each one's launch and prologue
  *          overlap its predecessor's tail (off in profiled calls).
  *          "graph" (0/1, default 1): run a single-GPU call as one CUDA graph launch whose round and

@@ -62,7 +62,7 @@ class RunStats(C.Structure):
                 ("iter_items", C.c_int64), ("launches", C.c_int64), ("iter_count_units", C.c_int64),
                 ("host_syncs", C.c_int64), ("ms_prep", C.c_double), ("ms_select", C.c_double),
                 ("ms_step_ctl", C.c_double), ("ms_merge", C.c_double), ("ms_assign", C.c_double),
-                ("ms_host_wait", C.c_double)]
+                ("ms_host_wait", C.c_double), ("guard_pairs", C.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

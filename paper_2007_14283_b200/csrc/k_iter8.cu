@@ -189,7 +189,11 @@ __device__ __forceinline__ uint32_t pack_w4(uint32_t d0, uint32_t d1, uint32_t d
 // (r2: 798 -> 762 cycles per tile at 2 seed tiles per frame, 790 -> 709 at 1; tools/k9_variants.sh)
 #define K8_RELEASE_C(cb) nbar_arrive(1 + (int)(cb), (kGroupWarps + 1) * 32)
 
-template <int DP>
+// GUARD (option "guard_stats", fms_run_stats.guard_pairs): also count the iteration pairs whose
+// similarity lies within the certified error bound of tau (kGuardEps), i.e. the window decisions the
+// 3-term fp32 similarity cannot certify against the exact one.  A separate instantiation: the
+// production kernel carries no extra instruction.
+template <int DP, bool GUARD = false>
 __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_constant__ TMaps tm, Params p) {
   using namespace k8;
   using Cfg = Iter8Cfg<DP>;
@@ -423,6 +427,8 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     // tau_m = the float just below 2^11 tau (C is scaled by 2^11, exactly)
     const float tau_m = __uint_as_float(__float_as_uint(p.tau_f * kLimb) - 1u);
+    unsigned long long gpairs = 0;  // GUARD: pairs within kGuardEps of tau (scaled by 2^11 like C)
+    (void)gpairs;
     uint32_t tcur = 0;                                // running tile index over the CTA's stream
     uint32_t mine = 0;                                // tiles handled by this group so far
     long long* gs = gsm + (size_t)grp * (DP * kBM) + row;  // this group's segment sums of this row, [k][kBM]
@@ -503,6 +509,14 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
               sub_tau2(v[4 * i], v[4 * i + 1], tau_m, d0, d1);
               sub_tau2(v[4 * i + 2], v[4 * i + 3], tau_m, d2, d3);
               pk[i] = pack_w4(d0, d1, d2, d3);
+              if constexpr (GUARD) {
+                if (w.mode == 0 && row < w.rows) {
+                  const long long px0 = (long long)(w.chunk * ct + (ctile - base)) * kBN + col + 4 * i;
+                  const float e = kGuardEps * kLimb;
+                  gpairs += (px0 + 0 < p.n && fabsf(__uint_as_float(d0)) < e) + (px0 + 1 < p.n && fabsf(__uint_as_float(d1)) < e) +
+                            (px0 + 2 < p.n && fabsf(__uint_as_float(d2)) < e) + (px0 + 3 < p.n && fabsf(__uint_as_float(d3)) < e);
+                }
+              }
             }
           } else {
 #pragma unroll
@@ -582,6 +596,10 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
       }
     }
     if (h == 0) flush();
+    if constexpr (GUARD) {
+      for (int o = 16; o > 0; o >>= 1) gpairs += __shfl_xor_sync(0xffffffffu, gpairs, o);
+      if (lane == 0 && gpairs) atomicAdd(reinterpret_cast<unsigned long long*>(p.counters + kGuardCounter), gpairs);
+    }
   }
 
   tc_fence_before();
@@ -593,6 +611,10 @@ __global__ void __launch_bounds__(k8::kThreads, 1) iter8_kernel(const __grid_con
 int iter8_smem_bytes(int DP) { return DP == 16 ? Iter8Cfg<16>::SMEM : Iter8Cfg<32>::SMEM; }
 
 cudaError_t launch_iter8(int DP, const TMaps& tm, const Params& p, int grid, cudaStream_t st) {
+  if (p.guard) {
+    if (DP == 16) return launch_ex(p.pdl, iter8_kernel<16, true>, grid, k8::kThreads, Iter8Cfg<16>::SMEM, st, tm, p);
+    return launch_ex(p.pdl, iter8_kernel<32, true>, grid, k8::kThreads, Iter8Cfg<32>::SMEM, st, tm, p);
+  }
   if (DP == 16) return launch_ex(p.pdl, iter8_kernel<16>, grid, k8::kThreads, Iter8Cfg<16>::SMEM, st, tm, p);
   return launch_ex(p.pdl, iter8_kernel<32>, grid, k8::kThreads, Iter8Cfg<32>::SMEM, st, tm, p);
 }
@@ -601,6 +623,8 @@ cudaError_t setup_iter8_attrs() {
   const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
   cudaError_t e = cudaFuncSetAttribute(iter8_kernel<16>, a, Iter8Cfg<16>::SMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(iter8_kernel<32>, a, Iter8Cfg<32>::SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(iter8_kernel<16, true>, a, Iter8Cfg<16>::SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(iter8_kernel<32, true>, a, Iter8Cfg<32>::SMEM);
   return e;
 }
 

@@ -123,6 +123,7 @@ struct Ctx {
   // device-resident loop (k_graph.cu): one CUDA graph per call configuration, cached
   int use_graph = 1;             // option "graph"
   int pdl = 1;                   // option "pdl": programmatic dependent launch of the step-loop kernels
+  int guard_stats = 0;           // option "guard_stats": K2 counts pairs within kGuardEps of tau
   int fuse_step = 0;             // option "fuse_step": the graph's step tail as one kernel (post_step; slower, DESIGN)
   cudaStream_t gst[3] = {nullptr, nullptr, nullptr};  // capture streams (prologue, round body, step body)
   struct GraphEntry {
@@ -452,7 +453,8 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   p.labels = labels;
   p.num_sms = c->num_sms;
   p.item_tiles_max = kChunkMax;
-  p.pdl = c->pdl && !c->profile;  // profiled calls time K2 with events between plain launches  // r2: 16 / 32 / 48 / 64 tiles measured 1622 / 1720 / 1678 / 1625 frames/s
+  p.pdl = c->pdl && !c->profile;  // profiled calls time K2 with events between plain launches
+  p.guard = c->guard_stats;  // r2: 16 / 32 / 48 / 64 tiles measured 1622 / 1720 / 1678 / 1625 frames/s
 
   const size_t need = carve(p, nullptr);
   if (need > c->ws_bytes) {
@@ -706,7 +708,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
   }
   CU(cudaEventRecord(c->t1, st));
   CU(cudaMemcpyAsync(c->h_ctl, p.ctl, sizeof(FrameCtl) * B, cudaMemcpyDeviceToHost, st));
-  if (gmode) CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
+  if (gmode || p.guard) CU(cudaMemcpyAsync(c->h_counters, p.counters, kCounters * 4, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   ++syncs;
   CU(cudaGetLastError());
@@ -766,6 +768,7 @@ fms_status run_batch(Ctx* c, const float* emb, int32_t B, int64_t n, int32_t d, 
     rs->steps = steps;
     rs->launches = kernels;
     rs->host_syncs = syncs;
+    rs->guard_pairs = p.guard ? reinterpret_cast<const long long*>(c->h_counters + kGuardCounter)[0] : 0;
     if (c->profile) {
       for (int l = 0; l < launches; ++l) {
         const int* snap = c->h_prof + (size_t)l * kProfInts;
@@ -1031,6 +1034,11 @@ fms_status fms_set_option(void* ctx, const char* key, int64_t value) {
   if (!strcmp(key, "graph")) {  // 1: device-resident loop (one CUDA graph launch per call); 0: host-polled
     if (value < 0 || value > 1) return fail(c, FMS_E_INVALID, "graph must be 0 or 1");
     c->use_graph = (int)value;
+    return FMS_OK;
+  }
+  if (!strcmp(key, "guard_stats")) {  // 1: K2's guard-pair count (fms_run_stats.guard_pairs)
+    if (value < 0 || value > 1) return fail(c, FMS_E_INVALID, "guard_stats must be 0 or 1");
+    c->guard_stats = (int)value;
     return FMS_OK;
   }
   if (!strcmp(key, "pdl")) {  // 1: plan / K2 / update / ctl_step / step condition launched with PDL
