@@ -238,15 +238,32 @@ __device__ unsigned long long radix_kth(const Params& p, int f, int round, bool 
       if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      long long cum = 0;
-      for (int b = 0; b < 256; ++b) {
-        if (cum + hist[b] >= s_k) {
-          s_prefix |= (unsigned long long)b << shift;
-          s_k -= cum;
-          break;
+    // the bin holding the k-th key: warp 0 scans the 256 bins (8 per lane) instead of one thread
+    if (threadIdx.x < 32) {
+      const int l = threadIdx.x;
+      unsigned int h8[8];
+      unsigned long long part = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { h8[u] = hist[l * 8 + u]; part += h8[u]; }
+      unsigned long long incl = part;  // inclusive prefix of the lanes' 8-bin partial sums
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (l >= o) incl += y;
+      }
+      const long long k0 = s_k;
+      const unsigned long long excl = incl - part;
+      const bool mine = (long long)excl < k0 && (long long)incl >= k0;  // exactly one lane
+      if (mine) {
+        long long cum = (long long)excl;
+        for (int u = 0; u < 8; ++u) {
+          if (cum + h8[u] >= k0) {
+            s_prefix |= (unsigned long long)(l * 8 + u) << shift;
+            s_k = k0 - cum;
+            break;
+          }
+          cum += h8[u];
         }
-        cum += hist[b];
       }
     }
     mask |= 0xFFull << shift;

@@ -514,8 +514,9 @@ cudaError_t launch_post_step(cudaGraphConditionalHandle h, const Params& p, int 
 }
 
 cudaError_t launch_update(const Params& p, int num_sms, cudaStream_t st) {
-  // grid-stride over the step's tiles
-  return launch_ex(p.pdl, p.DP == 16 ? update_kernel<16> : update_kernel<32>, num_sms, kBM, 0, st, p);
+  // grid-stride over the step's tiles; 4 CTAs per SM so a step's tiles (~160 at 96 frames) each get
+  // their own CTA instead of some CTAs running two tiles' dependent-load chains back to back
+  return launch_ex(p.pdl, p.DP == 16 ? update_kernel<16> : update_kernel<32>, 4 * num_sms, kBM, 0, st, p);
 }
 cudaError_t launch_ctl(const Params& p, cudaStream_t st) {
   return launch_ex(p.pdl, p.DP == 16 ? ctl_step_kernel<16> : ctl_step_kernel<32>, p.B, 256, 0, st, p);
