@@ -84,6 +84,7 @@ __device__ int merge_assemble(const Params& p, int f, unsigned long long* keys, 
 //    centres live in SMEM, so the serial in-batch chain never waits on global memory
 template <int DP>
 __device__ void merge_nms(const Params& p, int f, const int* vals, int P, float* cand, float* keptv) {
+  static_assert(32 * DP <= 1024, "one prefetched candidate value per thread of a 1024-thread CTA");
   FrameCtl& c = p.ctl[f];
   __shared__ unsigned s_supp;
   __shared__ unsigned s_inb[32];  // in-batch conflicts: bit j of s_inb[i] = candidate j (< i) within rho
@@ -105,15 +106,23 @@ __device__ void merge_nms(const Params& p, int f, const int* vals, int P, float*
   if (threadIdx.x == 0) { s_kept = 0; s_err = 0; }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // a batch's candidates (32 x DP floats, one per thread: blockDim >= 32 DP) are fetched during the
+  // previous batch, so no batch starts on a dependent global load
+  const int t = threadIdx.x;
+  auto fetch = [&](int b0) -> float {
+    const int nbb = min(32, P - b0);
+    if (b0 >= P || t >= nbb * DP) return 0.f;
+    const int ci = t / DP, q = t - ci * DP;
+    return pool[(size_t)vals[b0 + ci] * DP + q];
+  };
+  float cur = fetch(0);
   for (int base = 0; base < P; base += 32) {
     const int nb = min(32, P - base);
     if (threadIdx.x == 0) s_supp = 0;
     if (threadIdx.x < 32) s_inb[threadIdx.x] = 0;
-    for (int t = threadIdx.x; t < nb * DP; t += blockDim.x) {
-      const int ci = t / DP, q = t - ci * DP;
-      cand[t] = pool[(size_t)vals[base + ci] * DP + q];
-    }
+    if (t < nb * DP) cand[t] = cur;
     __syncthreads();
+    cur = fetch(base + 32);  // the next batch, in flight while this one is compared
     const int kept = s_kept;
     const int total = nb * kept;
     for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
