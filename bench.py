@@ -610,7 +610,8 @@ def main():
         "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
         "vs_baseline": None,
-        "dtype": "f16x3 split / f32 accumulate (similarity), u8 x s8 -> s32 exact (weighted sum)", "data": "synthetic",
+        "dtype": "f16x3 split / f32 accumulate (similarity), "
+                 + ("f16 weights x f16 limbs -> f32 (weighted sum)" if gauss else "u8 x s8 -> s32 exact (weighted sum)"), "data": "synthetic",
         "config": {"workload": f"{args.config}: {f0.H}x{f0.W} frame, {d}-D, {f0.cells} touching/overlapping cells "
                                f"+ background, full OSOP (N_initial 128, gamma 0.9, L 2, P 0.99)"
                                + (", Gaussian kernel profile (NEXT-4)" if gauss else "")
