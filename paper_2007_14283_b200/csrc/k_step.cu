@@ -519,7 +519,7 @@ cudaError_t launch_update(const Params& p, int num_sms, cudaStream_t st) {
   return launch_ex(p.pdl, p.DP == 16 ? update_kernel<16> : update_kernel<32>, 4 * num_sms, kBM, 0, st, p);
 }
 cudaError_t launch_ctl(const Params& p, cudaStream_t st) {
-  return launch_ex(p.pdl, p.DP == 16 ? ctl_step_kernel<16> : ctl_step_kernel<32>, p.B, 256, 0, st, p);
+  return launch_ex(p.pdl, p.DP == 16 ? ctl_step_kernel<16> : ctl_step_kernel<32>, p.B, 512, 0, st, p);
 }
 
 }  // namespace fms
