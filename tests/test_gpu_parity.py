@@ -392,3 +392,38 @@ def test_c4_paper_defaults_no_capacity_error():
     assert 0 < Kg[0] <= 8192 and lg[0].min() >= 0 and lg[0].max() < Kg[0]
     assert fr["seeds_total"] > 2048 and fr["rounds"] >= 3
     assert np.abs(np.linalg.norm(cg[0, :Kg[0]], axis=1) - 1.0).max() <= 1e-5
+
+
+def _degenerate(case):
+    rng = np.random.default_rng(41)
+    d = 16
+    if case == "identical":  # one direction, every pixel equal: one mode (Eq. 8's mean of equal vectors)
+        v = rng.standard_normal(d)
+        return np.tile(v / np.linalg.norm(v), (300, 1)).astype(np.float32), 0.1
+    if case == "repeated_tiny_h":  # 24 directions x 12 exact copies, h = 0.002: each direction its own mode
+        dirs = rng.standard_normal((24, d))
+        dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+        X = np.repeat(dirs, 12, axis=0)[rng.permutation(288)]
+        return X.astype(np.float32), 0.002
+    if case == "antipodal":  # +v and -v clusters (cosine -1 between them)
+        v = rng.standard_normal(d)
+        v /= np.linalg.norm(v)
+        X = np.concatenate([v + 0.02 * rng.standard_normal((150, d)), -v + 0.02 * rng.standard_normal((150, d))])
+        return X[rng.permutation(300)].astype(np.float32), 0.1
+    # large bandwidth: three orthogonal clusters at h = 0.5 (cross-cluster cosine ~0, far below tau = 0.5)
+    X = np.concatenate([np.eye(d)[k] + 0.02 * rng.standard_normal((100, d)) for k in range(3)])
+    return X[rng.permutation(300)].astype(np.float32), 0.5
+
+
+@pytest.mark.parametrize("case", ["identical", "repeated_tiny_h", "antipodal", "large_h"])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_degenerate_inputs_exact(case, kind):
+    """Degenerate inputs (SURVEY 8(c) edge cases): constructed so that no window decision lies near tau,
+    hence exact agreement with the oracle -- K, labels up to a bijection, centres, per-round trace."""
+    X, h = _degenerate(case)
+    pol = dict(kind=kind, n_seeds=64) if kind == 0 else dict(n_seeds=16)
+    xn = X.astype(np.float64) / np.linalg.norm(X.astype(np.float64), axis=1, keepdims=True)
+    assert np.min(np.abs(xn @ xn.T - (1.0 - h))) > 1e-4  # the construction keeps every pair off the boundary
+    lg, cg, Kg, st, ro = check_exact(X, h=h, **pol)
+    want = {"identical": 1, "repeated_tiny_h": 24, "antipodal": 2, "large_h": 3}[case]
+    assert Kg[0] == want, (case, Kg[0])
