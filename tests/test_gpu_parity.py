@@ -427,3 +427,46 @@ def test_degenerate_inputs_exact(case, kind):
     lg, cg, Kg, st, ro = check_exact(X, h=h, **pol)
     want = {"identical": 1, "repeated_tiny_h": 24, "antipodal": 2, "large_h": 3}[case]
     assert Kg[0] == want, (case, Kg[0])
+
+
+def test_c5_full_stack_properties():
+    """BASELINE configs[4] at full size (92 x 512x512 = 24.1M pixels clustered jointly, too large for the
+    oracle): properties that hold at any size.  (1) Every centre is a fixed point of the
+    mean-shift update (Eq. 8 / Alg. 2 l.4-9) over ALL pixels: the normalised mean of its flat window,
+    recomputed in fp64 on the host, lies within the convergence tolerance h/1000 of it.  (2) Sampled
+    pixels carry the label of their most similar centre (Alg. 2 l.12-14, lowest index on ties; pixels
+    whose top two similarities are within 1e-5 are skipped)."""
+    import torch
+    emb, truth = synth.make_stack(92, seed=0)
+    n = emb.shape[0]
+    h = 0.1
+    fms = _fms()
+    x = torch.from_numpy(emb).cuda()
+    pol = fms.default_policy(min_instance_px=min_instance_px(512 * 512) * 92, saturation_stop=1)
+    labels, centres, K, st = fms.cluster(x, h=h, policy=pol, centres_cap=4096)
+    torch.cuda.synchronize()
+    K = int(K[0])
+    C = centres[0, :K].cpu().numpy().astype(np.float64)
+    lab = labels[0].cpu().numpy()
+    del x, labels, centres
+    torch.cuda.empty_cache()
+    assert 20 <= K <= 200
+    # (1) fixed points, window sums over every pixel in fp64 (chunks of 2M pixels)
+    G = np.zeros_like(C)
+    for i0 in range(0, n, 2_000_000):
+        xc = emb[i0:i0 + 2_000_000].astype(np.float64)
+        xc /= np.linalg.norm(xc, axis=1, keepdims=True)
+        W = (xc @ C.T) >= 1.0 - h
+        G += W.T.astype(np.float64) @ xc
+    m = G / np.linalg.norm(G, axis=1, keepdims=True)
+    assert np.max(np.linalg.norm(m - C, axis=1)) <= 1.5 * h / 1000
+    # (2) nearest-centre labels on a sample
+    rng = np.random.default_rng(0)
+    idx = rng.choice(n, size=200_000, replace=False)
+    xs = emb[idx].astype(np.float64)
+    xs /= np.linalg.norm(xs, axis=1, keepdims=True)
+    S = xs @ C.T
+    top2 = np.sort(S, axis=1)[:, -2:]
+    clear = (top2[:, 1] - top2[:, 0]) > 1e-5
+    assert clear.mean() > 0.99
+    assert np.array_equal(lab[idx][clear], np.argmax(S, axis=1)[clear])
